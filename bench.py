@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FFT-convolution distance transform (contract: see DESIGN.md §Measurement).
+
+Default workload = BASELINE.json configs[1] ("C2"): signed distance + Hessian
+on a 2048^2 grid — S, grad S, (S_xx, S_yy, S_xy), winding number mu and the
+interior mask, tau = 0.5, float64 — from the seeded synthetic star curve
+(workloads.c2).  Metric: grid points per second (whole job, all ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C1..C5]
+
+One process per GPU (torchrun for N > 1).  C1-C3 do not shard: N ranks run N
+independent replicas ("weak").  C5 shards its 512 items across ranks with no
+communication ("strong").  `--impl reference` times the CPU oracle
+(oracle/eikfld_oracle.py, a bit-exact restatement of the reference's float64
+path) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+CONFIG_TEXT = {
+    "C1": "2D 256^2, K=2000 random nodes, tau=0.5: S + grad S",
+    "C2": "2D 2048^2 star curve (16384 vertices, 5908 distinct nodes), tau=0.5: S + grad S + Hessian + winding sign",
+    "C3": "3D 256^3, 16 ellipsoids x 12500 points (105389 distinct nodes), tau=0.5: S + grad S",
+    "C5": "batched 2D: 512 items x 512^2, K=1000 nodes each, tau=0.5: S + grad S per item",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIG_TEXT))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--items", type=int, default=512, help="C5 batch size (whole job)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- workloads
+
+
+def build_workload(cfg, seed, rank=0, world=1, items=512):
+    from paper_1112_3010_b200 import workloads as wl
+    from paper_1112_3010_b200.sign import FluxData, TangentData
+
+    if cfg == "C1":
+        d = wl.c1(seed)
+        return dict(grid=d["grid"], tau=d["tau"], nodes=[d["points"].distinct_nodes()], grad=True)
+    if cfg == "C2":
+        d = wl.c2(seed)
+        td = TangentData.build(d["curve"], d["grid"])
+        return dict(grid=d["grid"], tau=d["tau"], nodes=[d["points"].distinct_nodes()], grad=True, hess=True,
+                    sign=(td.nodes, np.ascontiguousarray(td.weights)), curve=d["curve"])
+    if cfg == "C3":
+        d = wl.c3(seed)
+        return dict(grid=d["grid"], tau=d["tau"], nodes=[d["points"].distinct_nodes()], grad=True)
+    if cfg == "C5":
+        per = items // world
+        d = wl.c5(seed, items=per, first=rank * per)
+        return dict(grid=d["grid"], tau=d["tau"], nodes=[p.distinct_nodes() for p in d["items"]], grad=True,
+                    items_total=per * world)
+    raise ValueError(cfg)
+
+
+def algorithmic_bytes(plan_info, w, batch):
+    """Compulsory HBM bytes per launch of each pass (DESIGN.md §Roofline model).
+
+    2-D, c0 x c1 grid, H = M1/2+1 spectral columns, kernel spectra folded to
+    (M0/2+1) x H doubles:  col = n_k*8*(M0/2+1)*H + n_c*16*c0*H ;
+    row = n_c*16*c0*H + (8*n_f64_out + n_u8_out)*N.
+    """
+    grid = w["grid"]
+    if len(grid.counts) != 2:
+        return {}
+    c0, c1 = grid.counts
+    M0 = plan_info["padded"][0]
+    H = plan_info["lines"]
+    dim = 2
+    n_dist = 1 + (dim if w.get("grad") else 0) + (3 if w.get("hess") else 0)
+    ks = (M0 // 2 + 1) * H * 8
+    out = {"col": batch * n_dist * 16 * c0 * H + n_dist * ks}
+    n_c = n_dist
+    if w.get("sign") is not None:
+        out["col_sign"] = 16 * c0 * H + 2 * ks
+        n_c += 1
+    n_f64 = 1 + (dim if w.get("grad") else 0) + (3 if w.get("hess") else 0) + (1 if w.get("sign") is not None else 0)
+    n_u8 = 1 if w.get("sign") is not None else 0
+    out["row"] = batch * (n_c * 16 * c0 * H + (8 * n_f64 + n_u8) * c0 * c1)
+    return out
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU side
+
+
+def oracle_step(w):
+    """One pass of the reference algorithm (oracle port) over the workload; returns grid points done."""
+    import eikfld_oracle as orc
+
+    grid = w["grid"]
+    pts = 0
+    for nodes in w["nodes"]:
+        orc.phi_unchecked(nodes, grid.counts, grid.spacing, w["tau"])  # s_fft's convolution
+        if w.get("hess"):
+            orc.hessian_2d_unchecked(nodes, grid.counts, grid.spacing, w["tau"])  # ratio batch incl. gradient
+        elif w.get("grad"):
+            orc.gradient_unchecked(nodes, grid.counts, grid.spacing, w["tau"])
+        pts += grid.num_nodes
+    if w.get("curve") is not None:
+        orc.winding_field(w["curve"].vertices, grid.origin, grid.spacing, grid.counts)
+    return pts
+
+
+def cpu_time(w, steps, warmup, budget_s=None):
+    import scipy.fft as sfft
+
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    cores = os.cpu_count() or 1
+    with sfft.set_workers(cores):
+        for _ in range(warmup):
+            oracle_step(w)
+        t0 = time.perf_counter()
+        pts = 0
+        done = 0
+        for _ in range(steps):
+            pts += oracle_step(w)
+            done += 1
+            if budget_s is not None and time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+    return pts / dt, dt / done, done, cores
+
+
+# ---------------------------------------------------------------- GPU side
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        w = build_workload(a.config, a.seed, 0, 1, min(a.items, 8))
+        if a.config == "C5":
+            w["nodes"] = w["nodes"][:8]
+        # CPU has no warm-up effects worth W full steps of a ~10 s pipeline; one is run
+        val, sec, done, cores = cpu_time(w, a.steps, min(a.warmup, 1), budget_s=240.0)
+        line = {
+            "metric": "grid points/sec (S+grad S+sign)", "value": val, "unit": "grid_points/s", "n_gpus": a.gpus,
+            "steps": done, "warmup": min(a.warmup, 1), "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak" if a.config != "C5" else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": a.config, "desc": CONFIG_TEXT[a.config]},
+            "cpu_baseline": {"value": val, "unit": "grid_points/s", "cores": cores, "kind": "port",
+                             "sample": f"{done} step(s) of the oracle pipeline on {a.config}"
+                                       + (" (8 of 512 items per step)" if a.config == "C5" else "")
+                                       + f", scipy.fft workers={cores}"},
+            "e2e": {"value": val, "unit": "grid_points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return 0
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1112_3010_b200 import _native
+    from paper_1112_3010_b200.engine import field_bits
+
+    w = build_workload(a.config, a.seed, rank, world, a.items)
+    grid = w["grid"]
+    dim = len(grid.counts)
+    t_plan = time.perf_counter()
+    plan = _native.Plan(dim, grid.counts, grid.spacing, w["tau"],
+                        field_bits(dim, w.get("grad", False), w.get("hess", False), w.get("sign") is not None), local)
+    t_plan = time.perf_counter() - t_plan
+    info = plan.info()
+    B = len(w["nodes"])
+    N = grid.num_nodes
+    nodes_h = np.concatenate(w["nodes"]).astype(np.int64)
+    offs_h = np.cumsum([0] + [len(n) for n in w["nodes"]]).astype(np.int64) if B > 1 else None
+    sn_h, sw_h = (w["sign"] if w.get("sign") is not None else (None, None))
+
+    def dev_t(x):
+        return None if x is None else torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+    nodes_d, offs_d, sn_d, sw_d = dev_t(nodes_h), dev_t(offs_h), dev_t(sn_h), dev_t(sw_h)
+    f64 = lambda: torch.empty(B * N, dtype=torch.float64, device=dev)  # noqa: E731
+    outs = {"S": f64()}
+    if w.get("grad"):
+        outs["grad"] = [f64() for _ in range(dim)]
+    if w.get("hess"):
+        outs["hess"] = [f64() for _ in range(3)]
+    if sn_d is not None:
+        outs["mu"] = f64()
+        outs["mask"] = torch.empty(B * N, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=False):
+        plan.run(nodes_d, offs_d, B, sn_d, sw_d, S=outs["S"], grad=outs.get("grad", (None,) * 3),
+                 hess=outs.get("hess", (None,) * 3), mu=outs.get("mu"), mask=outs.get("mask"),
+                 host=False, stream=stream.cuda_stream, profile=profile)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    pass_ms = {}
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            flush.fill_(float(i))  # evict L2 between timed steps (outside the events)
+            ev[i][0].record(stream)
+            step(profile=True)
+            ev[i][1].record(stream)
+            for k, v in plan.pass_times().items():
+                pass_ms.setdefault(k, []).append(v)
+        torch.cuda.synchronize()
+    total_ms = sum(s.elapsed_time(e) for s, e in ev)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    pts_per_step_job = B * N * world
+    value = pts_per_step_job * a.steps / (total_ms / 1e3)
+
+    # ---- end to end through the C-ABI with pinned HOST buffers
+    def pinned(n, dtype):
+        return torch.empty(n, dtype=dtype, pin_memory=True).numpy()
+
+    nodes_p = pinned(nodes_h.size, torch.int64)
+    nodes_p[:] = nodes_h
+    offs_p = None
+    if offs_h is not None:
+        offs_p = pinned(offs_h.size, torch.int64)
+        offs_p[:] = offs_h
+    sn_p = sw_p = None
+    if sn_h is not None:
+        sn_p = pinned(sn_h.size, torch.int64)
+        sn_p[:] = sn_h
+        sw_p = pinned(sw_h.size, torch.float64).reshape(sw_h.shape)
+        sw_p[:] = sw_h
+    ho = {"S": pinned(B * N, torch.float64)}
+    d2h = B * N * 8
+    if w.get("grad"):
+        ho["grad"] = [pinned(B * N, torch.float64) for _ in range(dim)]
+        d2h += dim * B * N * 8
+    if w.get("hess"):
+        ho["hess"] = [pinned(B * N, torch.float64) for _ in range(3)]
+        d2h += 3 * B * N * 8
+    if sn_h is not None:
+        ho["mu"] = pinned(N, torch.float64)
+        ho["mask"] = pinned(N, torch.uint8)
+        d2h += N * 9
+    h2d = nodes_h.nbytes + (offs_h.nbytes if offs_h is not None else 16) + \
+        ((sn_h.nbytes + sw_h.nbytes + 16) if sn_h is not None else 0)
+
+    def e2e_step():
+        plan.run(nodes_p, offs_p, B, sn_p, sw_p, S=ho["S"], grad=ho.get("grad", (None,) * 3),
+                 hess=ho.get("hess", (None,) * 3), mu=ho.get("mu"), mask=ho.get("mask"),
+                 host=True, stream=stream.cuda_stream)
+
+    for _ in range(max(1, min(a.warmup, 3))):
+        e2e_step()
+    ke = max(3, min(a.steps, 10))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ke):
+        flush.fill_(1.0)
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = pts_per_step_job * ke / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant pass
+    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback"
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
+    mean_pass = {k: float(np.mean(v)) for k, v in pass_ms.items()}
+    alg = algorithmic_bytes(info, w, B)
+    dom = max((k for k in mean_pass if k in alg), key=lambda k: mean_pass[k], default=None)
+    roof = None
+    if dom:
+        ach = alg[dom] / (mean_pass[dom] / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(REPO, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(a.config, {}).get(dom)
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": traffic, "kernel": dom, "algorithmic_bytes": alg[dom],
+                "kernel_ms": round(mean_pass[dom], 5), "peak_source": peak_src,
+                "step_bytes": sum(alg.values()),
+                "step_frac": round(sum(alg.values()) / (total_ms / a.steps / 1e3) / 1e9 / peak, 4)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        wc = dict(w)
+        if a.config == "C5":
+            wc["nodes"] = w["nodes"][:8]
+        v, sec, done, cores = cpu_time(wc, 1, 0)
+        cpu = {"value": v, "unit": "grid_points/s", "cores": cores, "kind": "port",
+               "sample": f"1 step of the oracle pipeline on {a.config}" + (" (8 items)" if a.config == "C5" else "")
+                         + f" ({sec:.1f} s), scipy.fft workers={cores}"}
+
+    launches_per_step = {"C1": 5, "C2": 7, "C3": 6, "C5": 5}[a.config]
+    if rank == 0:
+        line = {
+            "metric": "grid points/sec (S+grad S+sign)", "value": value, "unit": "grid_points/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
+            "scaling": "strong" if a.config == "C5" else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators of BASELINE.json configs, workloads.py)",
+            "config": {"workload": a.config, "desc": CONFIG_TEXT[a.config], "grid": list(grid.counts),
+                       "batch_per_rank": B, "padded": list(info["padded"]), "l2": "flushed between timed steps",
+                       "parallelism": "replicas" if a.config != "C5" else f"batch-shard x{world}",
+                       "plan_build_s": round(t_plan, 3)},
+            "e2e": {"value": e2e_val, "unit": "grid_points/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": ke},
+            "gpu_launches": launches_per_step * a.steps,
+            "pass_ms": {k: round(v, 5) for k, v in mean_pass.items()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,128 @@
+/* eikfld_b200 — C ABI of the B200-native FFT-convolution distance transform.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `eikfld` (/root/reference/pkg/src/eikfld).  The reference is pure Python and
+ * has no FFI of its own; its "operator API" for this path is the module API
+ * listed below.  Each entry point names the reference functions whose work it
+ * replaces (file:line, R/ = /root/reference/pkg/src/eikfld/).  The Python
+ * package `paper_1112_3010_b200` binds these with ctypes and re-exposes the
+ * reference signatures (see INTEGRATION.md for the binding a maintainer of the
+ * reference would add).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no exceptions cross the ABI;
+ *   - fields are float64, row-major (last axis fastest), N = prod(counts) per grid;
+ *   - node lists are flat indices (np.ravel_multi_index order), strictly
+ *     increasing within each item (np.unique order, R/grid.py:112-114);
+ *   - by default every pointer is a device pointer and work is queued on
+ *     `stream` (a cudaStream_t, NULL = legacy default stream) without a host
+ *     sync; EIK_HOST_INPUTS / EIK_HOST_OUTPUTS make the library stage host
+ *     buffers itself (pinned host memory gives the best copy rate);
+ *   - status codes: 0 ok, 1 validation, 2 underflow (phi <= 0 somewhere;
+ *     only reported when EIK_CHECK_UNDERFLOW is set), 3 CUDA/OOM;
+ *   - a plan is reentrant for calls on one stream at a time; distinct plans are
+ *     independent.  No floating-point atomics are used on value paths, so
+ *     results are bit-reproducible run to run.
+ */
+#ifndef EIKFLD_B200_H
+#define EIKFLD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIK_OK 0
+#define EIK_EVALIDATION 1
+#define EIK_EUNDERFLOW 2
+#define EIK_ECUDA 3
+
+/* plan field bits: which kernel spectra a plan caches */
+#define EIK_FIELD_PHI 0x1u     /* phi = exp(-|x|/tau) * delta_Y      R/distance.py:63-86   */
+#define EIK_FIELD_S 0x2u       /* S = -tau log phi                   R/distance.py:89-122  */
+#define EIK_FIELD_GRAD 0x4u    /* grad S ratios                      R/derivatives.py:64-79,156-172 */
+#define EIK_FIELD_HESS 0x8u    /* (S_xx, S_yy, S_xy), 2-D only       R/derivatives.py:82-112 */
+#define EIK_FIELD_WINDING 0x10u /* winding number mu, 2-D           R/sign.py:108-132 */
+#define EIK_FIELD_DEGREE 0x20u /* topological degree mu, 3-D        R/sign.py:135-163 */
+
+/* run flags */
+#define EIK_HOST_INPUTS 0x1u
+#define EIK_HOST_OUTPUTS 0x2u
+#define EIK_SYNC 0x4u              /* synchronize the stream before returning */
+#define EIK_CHECK_UNDERFLOW 0x8u   /* sync, and return EIK_EUNDERFLOW if any phi <= 0
+                                      (R/convolution.py:378-388 assert_positive) */
+#define EIK_PROFILE 0x10u          /* record CUDA events around each pass (see eik_pass_times) */
+
+/* pass ids reported by eik_pass_times */
+#define EIK_PASS_PREP 0     /* node validation + per-row CSR */
+#define EIK_PASS_COL 1      /* fused column kernel, distance group (impulse DFT, fwd, multiply, inverses) */
+#define EIK_PASS_COL_SIGN 2 /* fused column kernel, sign group */
+#define EIK_PASS_LINES 3    /* 3-D inverse along axis 1 */
+#define EIK_PASS_ROW 4      /* c2r along the last axis + epilogue */
+#define EIK_NPASS 5
+
+typedef struct eik_plan eik_plan;
+
+typedef struct {
+  /* unit impulses delta_Y (R/distance.py:50-60): sorted distinct flat nodes */
+  const int64_t* nodes;
+  const int64_t* item_offsets; /* batch+1 offsets into nodes; NULL when batch == 1 */
+  int64_t n_nodes;             /* total nodes over all items */
+  int64_t batch;               /* independent grids sharing this plan (>= 1) */
+  /* weighted impulses for the sign field: sorted distinct flat nodes and
+     dim weight rows (weights[a*n_sign_nodes + p]); 2-D: chord tangents
+     accumulated per node (R/sign.py:42-57); 3-D: area-weighted normals
+     accumulated per node (R/sign.py:68-86).  Batch 1 only. */
+  const int64_t* sign_nodes;
+  int64_t n_sign_nodes;
+  const double* sign_weights;
+} eik_inputs;
+
+typedef struct {
+  /* every pointer may be NULL (not computed); sizes are batch * N */
+  double* phi;        /* raw convolution phi */
+  double* S;          /* -tau log phi, NaN where phi <= 0 */
+  double* grad[3];    /* S_a = (f_a exp * delta)/(exp * delta), reference axis order */
+  double* hess[3];    /* S_xx, S_yy, S_xy (2-D) */
+  double* mu;         /* winding (2-D) or degree (3-D) field */
+  uint8_t* mask;      /* rint(mu) > 0 (2-D) / rint(mu) >= 1 (3-D), unflagged rule of R/sign.py:190-195 */
+  uint8_t* underflow; /* 1 where phi <= 0 */
+  int64_t* n_underflow;        /* host scalar, written when the call synchronizes */
+  unsigned long long* d_underflow_count; /* optional device counter (accumulated) */
+} eik_outputs;
+
+/* Build a plan for a grid: padded lengths, twiddles and the cached kernel
+ * spectra for `fields` (replaces the per-call kernel sampling + forward FFTs of
+ * R/distance.py:22-47, R/derivatives.py:26-57,139-153, R/sign.py:97-105 and
+ * FftConvolver.__init__/kernel_hat, R/convolution.py:220-251). */
+int eik_plan_create(int dim, const int64_t* counts, double spacing, double tau, uint32_t fields,
+                    int device, eik_plan** out);
+int eik_plan_destroy(eik_plan* plan);
+/* padded[3], spectral lines per item, device bytes held */
+int eik_plan_info(const eik_plan* plan, int64_t* padded, int64_t* lines, int64_t* device_bytes);
+
+/* One pass of the hot path over a batch: phi, S, gradient, Hessian from one
+ * shared transform of delta_Y plus the sign field (R/distance.py:114-122,
+ * R/derivatives.py:64-112, R/sign.py:108-163). */
+int eik_run(eik_plan* plan, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream);
+
+/* Engine-level linear convolution of n_kernels centred kernels (each of shape
+ * kshape, odd, >= 2c-1 per axis) with one dense field on the grid
+ * (FftConvolver.convolve/convolve_many, R/convolution.py:317-366).  kernels:
+ * n_kernels * prod(kshape) doubles; field: N doubles; out: n_kernels * N. */
+int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t n_kernels,
+                 const int64_t* kshape, const double* field, double* out, uint32_t flags, int device,
+                 void* stream);
+
+/* Device milliseconds of each pass of the last eik_run issued with
+ * EIK_PROFILE (synchronizes on its events); -1 for passes that did not run. */
+int eik_pass_times(eik_plan* plan, double* ms, int n);
+
+const char* eik_last_error(void);
+int eik_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EIKFLD_B200_H */

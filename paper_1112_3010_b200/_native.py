@@ -1,0 +1,216 @@
+"""ctypes binding of libeikfld_b200.so (the C ABI in include/eikfld_b200.h).
+
+The library is built in-tree (`python -c "import __graft_entry__ as g; g.build()"`
+or `make`).  There is no fallback: if the shared object is missing or no CUDA
+device is visible, every entry point raises NativeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from collections import OrderedDict
+
+import numpy as np
+
+from .errors import NativeError, PrecisionError, ValidationError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libeikfld_b200.so")
+
+EIK_OK, EIK_EVALIDATION, EIK_EUNDERFLOW, EIK_ECUDA = 0, 1, 2, 3
+FIELD_PHI, FIELD_S, FIELD_GRAD, FIELD_HESS, FIELD_WINDING, FIELD_DEGREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+HOST_INPUTS, HOST_OUTPUTS, SYNC, CHECK_UNDERFLOW, PROFILE = 0x1, 0x2, 0x4, 0x8, 0x10
+PASS_NAMES = ("prep", "col", "col_sign", "lines", "row")
+
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class Inputs(C.Structure):
+    _fields_ = [
+        ("nodes", C.c_void_p), ("item_offsets", C.c_void_p), ("n_nodes", C.c_int64), ("batch", C.c_int64),
+        ("sign_nodes", C.c_void_p), ("n_sign_nodes", C.c_int64), ("sign_weights", C.c_void_p),
+    ]
+
+
+class Outputs(C.Structure):
+    _fields_ = [
+        ("phi", C.c_void_p), ("S", C.c_void_p), ("grad", C.c_void_p * 3), ("hess", C.c_void_p * 3),
+        ("mu", C.c_void_p), ("mask", C.c_void_p), ("underflow", C.c_void_p),
+        ("n_underflow", C.c_void_p), ("d_underflow_count", C.c_void_p),
+    ]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load the shared library once; raise NativeError when it is unavailable."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeError(
+                    f"CUDA library not built ({LIB_PATH} missing); run `make` or __graft_entry__.build()"
+                )
+            L = C.CDLL(LIB_PATH)
+            L.eik_plan_create.argtypes = [C.c_int, _i64p, C.c_double, C.c_double, C.c_uint32, C.c_int, C.POINTER(C.c_void_p)]
+            L.eik_plan_destroy.argtypes = [C.c_void_p]
+            L.eik_plan_info.argtypes = [C.c_void_p, _i64p, _i64p, _i64p]
+            L.eik_run.argtypes = [C.c_void_p, C.POINTER(Inputs), C.POINTER(Outputs), C.c_uint32, C.c_void_p]
+            L.eik_convolve.argtypes = [C.c_int, _i64p, C.c_void_p, C.c_int64, _i64p, C.c_void_p, C.c_void_p,
+                                       C.c_uint32, C.c_int, C.c_void_p]
+            L.eik_pass_times.argtypes = [C.c_void_p, _f64p, C.c_int]
+            L.eik_last_error.restype = C.c_char_p
+            for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
+                         "eik_version", "eik_pass_times"):
+                getattr(L, name).restype = C.c_int
+            _lib = L
+        return _lib
+
+
+def exported_symbols():
+    return ["eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
+            "eik_pass_times", "eik_last_error", "eik_version"]
+
+
+def check(rc: int):
+    if rc == EIK_OK:
+        return
+    msg = lib().eik_last_error().decode(errors="replace")
+    if rc == EIK_EVALIDATION:
+        raise ValidationError(msg)
+    if rc == EIK_EUNDERFLOW:
+        raise PrecisionError(msg)
+    raise NativeError(msg)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch tensor (device or host)
+
+
+class Plan:
+    """Owns one eik_plan: geometry, twiddles and cached kernel spectra on one device."""
+
+    def __init__(self, dim, counts, spacing, tau, fields, device=0):
+        self.dim = int(dim)
+        self.counts = tuple(int(c) for c in counts)
+        self.spacing = float(spacing)
+        self.tau = float(tau)
+        self.fields = int(fields)
+        self.device = int(device)
+        self.N = int(np.prod(self.counts))
+        h = C.c_void_p()
+        cnt = (C.c_int64 * 3)(*self.counts, *([1] * (3 - len(self.counts))))
+        check(lib().eik_plan_create(self.dim, cnt, self.spacing, self.tau, self.fields, self.device, C.byref(h)))
+        self._h = h
+        self._lock = threading.Lock()
+
+    def info(self):
+        pad = (C.c_int64 * 3)()
+        lines = C.c_int64()
+        nbytes = C.c_int64()
+        check(lib().eik_plan_info(self._h, pad, C.byref(lines), C.byref(nbytes)))
+        return {"padded": tuple(pad), "lines": lines.value, "device_bytes": nbytes.value}
+
+    def pass_times(self):
+        """Device ms per pass of the last profiled run ({name: ms}, absent passes omitted)."""
+        ms = (C.c_double * len(PASS_NAMES))()
+        check(lib().eik_pass_times(self._h, ms, len(PASS_NAMES)))
+        return {n: v for n, v in zip(PASS_NAMES, ms) if v >= 0}
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().eik_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    __del__ = close
+
+    def run(self, nodes=None, item_offsets=None, batch=1, sign_nodes=None, sign_weights=None, *,
+            phi=None, S=None, grad=(None, None, None), hess=(None, None, None), mu=None, mask=None,
+            underflow=None, count=False, check_underflow=False, host=True, stream=None, profile=False):
+        """Run the hot path.  Arrays are numpy (host=True) or torch CUDA tensors (host=False)."""
+        inp = Inputs()
+        keep = []
+        if nodes is not None:
+            inp.nodes = _ptr(nodes)
+            inp.n_nodes = int(nodes.shape[0])
+            keep.append(nodes)
+        if item_offsets is not None:
+            inp.item_offsets = _ptr(item_offsets)
+            keep.append(item_offsets)
+        inp.batch = int(batch)
+        if sign_nodes is not None:
+            inp.sign_nodes = _ptr(sign_nodes)
+            inp.n_sign_nodes = int(sign_nodes.shape[0])
+            inp.sign_weights = _ptr(sign_weights)
+            keep += [sign_nodes, sign_weights]
+        out = Outputs()
+        out.phi, out.S, out.mu, out.mask, out.underflow = (_ptr(x) for x in (phi, S, mu, mask, underflow))
+        for d in range(3):
+            out.grad[d] = _ptr(grad[d]) if d < len(grad) else None
+            out.hess[d] = _ptr(hess[d]) if d < len(hess) else None
+        n_uf = C.c_int64(-1)
+        if count or check_underflow:
+            out.n_underflow = C.addressof(n_uf)
+        flags = (HOST_INPUTS | HOST_OUTPUTS) if host else 0
+        if check_underflow:
+            flags |= CHECK_UNDERFLOW
+        if profile:
+            flags |= PROFILE
+        with self._lock:
+            rc = lib().eik_run(self._h, C.byref(inp), C.byref(out), flags, stream)
+        check(rc)
+        return n_uf.value
+
+
+_PLANS: "OrderedDict[tuple, Plan]" = OrderedDict()
+_PLANS_LOCK = threading.Lock()
+_MAX_PLANS = 8
+
+
+def get_plan(grid, tau, fields, device=0) -> Plan:
+    """Plan cache keyed by (device, counts, spacing, tau, fields) — the analogue
+    of the reference's plan cache (R/convolution.py:70-71,105-112)."""
+    key = (device, tuple(grid.counts), float(grid.spacing), float(tau), int(fields))
+    with _PLANS_LOCK:
+        p = _PLANS.get(key)
+        if p is not None:
+            _PLANS.move_to_end(key)
+            return p
+    p = Plan(len(grid.counts), grid.counts, grid.spacing, tau, fields, device)
+    with _PLANS_LOCK:
+        _PLANS[key] = p
+        while len(_PLANS) > _MAX_PLANS:
+            _, old = _PLANS.popitem(last=False)
+            old.close()
+    return p
+
+
+def clear_plans():
+    with _PLANS_LOCK:
+        for p in _PLANS.values():
+            p.close()
+        _PLANS.clear()
+
+
+def convolve(counts, kernels, field, device=0):
+    """Host-in/host-out linear convolution of stacked centred kernels with a dense field."""
+    counts = tuple(int(c) for c in counts)
+    kernels = np.ascontiguousarray(kernels, dtype=np.float64)
+    field = np.ascontiguousarray(field, dtype=np.float64).reshape(-1)
+    n = kernels.shape[0]
+    kshape = kernels.shape[1:]
+    out = np.empty((n, int(np.prod(counts))), dtype=np.float64)
+    cnt = (C.c_int64 * 3)(*counts, *([1] * (3 - len(counts))))
+    ks = (C.c_int64 * 3)(*kshape, *([1] * (3 - len(kshape))))
+    check(lib().eik_convolve(len(counts), cnt, kernels.ctypes.data, n, ks, field.ctypes.data, out.ctypes.data,
+                             HOST_INPUTS | HOST_OUTPUTS, device, None))
+    return out

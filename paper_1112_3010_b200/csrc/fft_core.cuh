@@ -1,0 +1,198 @@
+// fp64 complex FFT building blocks for sm_100a.
+//
+// Shape of the engine
+// -------------------
+// A "line" is one 1-D transform of length M = 2^L.  It is computed by TPL
+// threads, each holding EPT = 16 complex values in registers (EPT = M for
+// L <= 4).  Stages are Stockham radix-R steps (R in {2,4,8,16}); between
+// stages the line is exchanged through a padded shared-memory buffer.  The
+// forward schedule is [R0, 16, 16, ...] (R0 absorbs L mod 4); the inverse
+// schedule is its reverse, which makes the register layout of a forward
+// result identical to the register layout an inverse expects as input: the
+// spectral multiply happens in registers with no shared-memory round trip.
+//
+// Register i of thread t maps to line element
+//   fwd input  / inv output : (t + (i / R0) * TPL) + (i % R0) * (M / R0)
+//   fwd output / inv input  : (t + (i / RL) * TPL) + (i % RL) * (M / RL)
+// (RL = last forward radix).  Zero-padded inputs (only the first M/2
+// elements non-zero) and half-length outputs (only the first M/2 needed) are
+// pruned inside the first/last radix step.
+//
+// Twiddles come from one correctly rounded table W_MAX^j = exp(-2 pi i j / MAX)
+// per plan (read through the read-only path); inverse transforms use its
+// conjugate.  No normalisation is applied anywhere: callers fold the exact
+// power-of-two scale into their epilogue.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eik {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// a * w
+__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
+  return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
+}
+// a * conj(w)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 w) {
+  return make_double2(fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y));
+}
+
+constexpr double kC1 = 0.92387953251128675613;  // cos(pi/8)
+constexpr double kS1 = 0.38268343236508977173;  // sin(pi/8)
+constexpr double kR2 = 0.70710678118654752440;  // 1/sqrt(2)
+
+// a * W16^q   (forward W16 = exp(-2 pi i/16); inverse uses the conjugate)
+template <bool INV>
+__device__ __forceinline__ double2 w16(double2 a, int q) {
+  const double sg = INV ? -1.0 : 1.0;  // sign of the imaginary part of conj-ness
+  switch (q) {
+    case 0: return a;
+    case 4: return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+    case 2: return INV ? make_double2((a.x - a.y) * kR2, (a.x + a.y) * kR2)
+                       : make_double2((a.x + a.y) * kR2, (a.y - a.x) * kR2);
+    case 6: return INV ? make_double2(-(a.x + a.y) * kR2, (a.x - a.y) * kR2)
+                       : make_double2((a.y - a.x) * kR2, -(a.x + a.y) * kR2);
+    default: {
+      double c, s;  // W16^q = c - i*s (forward)
+      if (q == 1) { c = kC1; s = kS1; }
+      else if (q == 3) { c = kS1; s = kC1; }
+      else if (q == 5) { c = -kS1; s = kC1; }
+      else { c = -kC1; s = kS1; }  // q == 7
+      s *= sg;
+      return make_double2(fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s));
+    }
+  }
+}
+
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+__host__ __device__ constexpr int bitrev(int n, int bits) {
+  return bits == 0 ? 0 : (((n & 1) << (bits - 1)) | bitrev(n >> 1, bits - 1));
+}
+
+// In-register R-point DFT (natural order in/out), radix-2 DIT, R <= 16.
+// HALF_IN: a[R/2..R) are known zero (not read).
+template <int R, bool INV, bool HALF_IN>
+__device__ __forceinline__ void dft(double2* a) {
+  if constexpr (R == 1) {
+    return;
+  } else {
+    constexpr int B = ilog2c(R);
+    double2 x[R];
+#pragma unroll
+    for (int n = 0; n < R; ++n) {
+      if (!(HALF_IN && (n & 1))) x[n] = a[bitrev(n, B)];
+    }
+#pragma unroll
+    for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+      for (int s = 0; s < R; s += len) {
+#pragma unroll
+        for (int k = 0; k < len / 2; ++k) {
+          if (HALF_IN && len == 2) {
+            x[s + 1] = x[s];
+          } else {
+            double2 u = x[s + k];
+            double2 w = w16<INV>(x[s + k + len / 2], k * (16 / len));
+            x[s + k] = cadd(u, w);
+            x[s + k + len / 2] = csub(u, w);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < R; ++n) a[n] = x[n];
+  }
+}
+
+__device__ __forceinline__ int spad(int i) { return i + (i >> 3); }
+
+// Compile-time description of a length-2^L line transform.
+template <int L_>
+struct Line {
+  static constexpr int L = L_;
+  static constexpr int M = 1 << L;
+  static constexpr int EPT = (L <= 4) ? M : 16;
+  static constexpr int TPL = M / EPT;
+  static constexpr int NST = (L == 0) ? 0 : ((L <= 4) ? 1 : (L + 3) / 4);
+  static constexpr int R0 = (L <= 4) ? M : ((L % 4) ? (1 << (L % 4)) : 16);
+  static constexpr int RL = (NST <= 1) ? R0 : 16;
+  static constexpr int SMEM = M + (M >> 3) + 1;  // padded double2 slots per line
+  __host__ __device__ static constexpr int frad(int s) { return s == 0 ? R0 : 16; }
+  __host__ __device__ static constexpr int rad(bool inv, int s) { return inv ? frad(NST - 1 - s) : frad(s); }
+  __host__ __device__ static constexpr int ns(bool inv, int s) { return s == 0 ? 1 : ns(inv, s - 1) * rad(inv, s - 1); }
+  // element index held by register i of thread t
+  __device__ static __forceinline__ int in_idx(int t, int i) {   // forward input / inverse output
+    return (t + (i / R0) * TPL) + (i % R0) * (M / R0);
+  }
+  __device__ static __forceinline__ int out_idx(int t, int i) {  // forward output / inverse input
+    return (t + (i / RL) * TPL) + (i % RL) * (M / RL);
+  }
+  // register i is a structurally-zero input of a half-padded forward transform
+  __device__ static __forceinline__ constexpr bool upper_in(int i) { return (i % R0) >= (R0 / 2); }
+};
+
+// One Stockham stage S of direction INV, followed (if not last) by the
+// shared-memory exchange into the next stage's register layout.
+// tw: table of W_MAX^j, j in [0, MAX); lmax = log2(MAX).
+template <class LN, bool INV, int S, bool HALF_IN>
+__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm,
+                                      const double2* __restrict__ tw, int lmax) {
+  constexpr int R = LN::rad(INV, S);
+  constexpr int NS = LN::ns(INV, S);
+  constexpr int G = LN::EPT / R;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int b = t + g * LN::TPL;
+    if constexpr (NS > 1) {
+      const int k = b & (NS - 1);
+      const int sh = lmax - ilog2c(NS * R);
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const double2 w = __ldg(tw + ((k * r) << sh));
+        v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
+      }
+    }
+    dft<R, INV, HALF_IN && S == 0>(&v[g * R]);
+  }
+  if constexpr (S + 1 < LN::NST) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int b = t + g * LN::TPL;
+      const int o = (b / NS) * NS * R + (b & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[spad(o + r * NS)] = v[g * R + r];
+    }
+    __syncthreads();
+    constexpr int R2 = LN::rad(INV, S + 1);
+    constexpr int G2 = LN::EPT / R2;
+#pragma unroll
+    for (int g = 0; g < G2; ++g) {
+      const int b = t + g * LN::TPL;
+#pragma unroll
+      for (int r = 0; r < R2; ++r) v[g * R2 + r] = sm[spad(b + r * (LN::M / R2))];
+    }
+    __syncthreads();
+  }
+}
+
+template <class LN, bool INV, int S, bool HALF_IN>
+__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, double2* sm,
+                                            const double2* __restrict__ tw, int lmax) {
+  if constexpr (S < LN::NST) {
+    stage<LN, INV, S, HALF_IN>(v, t, sm, tw, lmax);
+    stages_from<LN, INV, S + 1, HALF_IN>(v, t, sm, tw, lmax);
+  }
+}
+
+// Full transform of the line held in v (layouts documented above).
+// HALF_IN (forward only): input elements >= M/2 are zero and their registers are not read.
+template <class LN, bool INV, bool HALF_IN = false>
+__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, double2* sm,
+                                         const double2* __restrict__ tw, int lmax) {
+  static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
+  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, sm, tw, lmax);
+}
+
+}  // namespace eik

@@ -1,0 +1,592 @@
+// Device kernels of the FFT-convolution distance transform (sm_100a, fp64).
+//
+// Pipeline (2D, grid c0 x c1, padded M0 x M1, half spectrum H1 = M1/2+1):
+//   prep_nodes / rowptr   sorted node list -> per-row CSR (deterministic)
+//   col_kernel<SPARSE>    per spectral column k1: impulse DFT along axis 1
+//                         straight from the node list (delta_Y never exists
+//                         in memory), forward FFT along axis 0, multiply by
+//                         the cached kernel spectra, one inverse FFT per
+//                         output component, keep rows [0,c0)          (K1-K5)
+//   row_kernel            per grid row: c2r along axis 1 (half-length
+//                         complex IFFT) fused with the epilogue
+//                         S=-tau log phi, S_a=num/phi, Hessian, mu, sign,
+//                         underflow flag/count                        (K5-K6)
+// 3D adds a plane pass (impulse DFT along axis 2 + FFT along axis 1, stored),
+// runs col_kernel<DENSE> along axis 0, and an inverse lines pass along axis 1
+// before the row kernel.  Kernel spectra are produced once per plan by
+// row_r2c_kernel + lines_kernel + col_kernel<DENSE, SPECTRUM> (K3).
+//
+// Thread mappings: "column" kernels (col/lines) are line-minor
+// (line = tid % LPC) so that a warp touches LPC adjacent lines at the same
+// element: every global access is a contiguous run across lines.  Row
+// kernels are line-major (a row is contiguous in memory).
+#pragma once
+#include "fft_core.cuh"
+
+namespace eik {
+
+constexpr int MAXC = 8;
+
+enum { IN_SPARSE = 0, IN_DENSE = 1 };
+enum { OUT_COMPS = 0, OUT_SUM = 1, OUT_SPECTRUM = 2 };
+enum { SPEC_COMPLEX = 0, SPEC_REAL_T = 1, SPEC_IMAG_T = 2, SPEC_COMPLEX_T = 3 };
+
+// Threads per CTA for a column kernel of length 2^L, and lines per CTA.
+__host__ __device__ constexpr int col_threads(int L) { return L >= 10 ? 512 : 256; }
+template <int L>
+struct ColCfg {
+  using LN = Line<L>;
+  static constexpr int NT = (col_threads(L) > LN::TPL) ? col_threads(L) : LN::TPL;
+  static constexpr int LPC = NT / LN::TPL;
+  static constexpr size_t SMEM_BYTES = (size_t)LPC * LN::SMEM * sizeof(double2);
+};
+template <int L>
+struct RowCfg {
+  using LN = Line<L>;
+  static constexpr int NT = (LN::TPL >= 128) ? LN::TPL : 128;
+  static constexpr int LPC = NT / LN::TPL;
+  static constexpr size_t SMEM_BYTES = (size_t)LPC * LN::SMEM * sizeof(double2);
+};
+
+// Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
+// folded along axis 0: re[k0 * ld + l], k0 in [0, M0/2]; K(M0-k0) = (odd0 ? -1 : 1) * K(k0).
+// General complex spectra (arbitrary user kernels): cplx[k0 * ld + l], k0 in [0, M0).
+struct KSpec {
+  const double* re;
+  const double2* cplx;
+  int64_t ld;
+  int imag;
+  int odd0;
+};
+
+struct ColArgs {
+  int64_t nlines;  // spectral lines per item
+  int n_valid;     // non-zero input elements per line
+  int n_out;       // outputs kept per line (inverse)
+  int n_in, n_comp;
+  // sparse impulse input (rows of the transform axis; last-axis coordinate + weights)
+  const int64_t* rowptr;
+  const int32_t* cols;
+  const double* w[3];
+  int64_t rows_per_item;
+  int last_shift;  // lmax - log2(M_last)
+  int last_mask;   // M_last - 1
+  // dense input din[i][item*din_item + e*din_es + l]
+  const double2* din[3];
+  int64_t din_es, din_item;
+  // kernel spectra (COMPS: one per component; SUM: one per input)
+  KSpec ks[MAXC];
+  // outputs out[j][item*out_item + n*out_es + l]
+  double2* out[MAXC];
+  int64_t out_es, out_item;
+  // spectrum extraction (OUT_SPECTRUM)
+  int spec_mode;
+  double* spec_re[3];
+  int64_t spec_ld;
+  const double2* tw;
+  int lmax;
+};
+
+__device__ __forceinline__ double2 kmul(double2 x, const KSpec& k, int64_t l, int k0, int M0) {
+  if (k.cplx) return cmul(x, __ldg(k.cplx + (int64_t)k0 * k.ld + l));
+  const int half = M0 >> 1;
+  const bool hi = k0 > half;
+  double v = __ldg(k.re + (int64_t)(hi ? M0 - k0 : k0) * k.ld + l);
+  if (hi && k.odd0) v = -v;
+  return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
+}
+
+template <class LN, int LPC, bool HALF>
+__device__ __forceinline__ void load_sparse(double2 (&v)[LN::EPT], const ColArgs& a, int t, int64_t l,
+                                            int64_t item, int inp, bool valid) {
+  const double* __restrict__ w = a.w[inp];
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
+    const int e = LN::in_idx(t, r);
+    double2 acc = make_double2(0.0, 0.0);
+    if (valid && e < a.n_valid) {
+      const int64_t row = item * a.rows_per_item + e;
+      const int64_t p0 = __ldg(a.rowptr + row), p1 = __ldg(a.rowptr + row + 1);
+      for (int64_t p = p0; p < p1; ++p) {
+        const int col = __ldg(a.cols + p);
+        const int idx = (int)(((int64_t)col * l) & a.last_mask) << a.last_shift;
+        const double2 tw = __ldg(a.tw + idx);
+        const double wt = w ? __ldg(w + p) : 1.0;
+        acc.x = fma(wt, tw.x, acc.x);
+        acc.y = fma(wt, tw.y, acc.y);
+      }
+    }
+    v[r] = acc;
+  }
+}
+
+template <class LN, bool HALF>
+__device__ __forceinline__ void load_dense(double2 (&v)[LN::EPT], const ColArgs& a, int t, int64_t l,
+                                           int64_t item, int inp, bool valid) {
+  const double2* __restrict__ src = a.din[inp] + item * a.din_item + l;
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
+    const int e = LN::in_idx(t, r);
+    v[r] = (valid && e < a.n_valid) ? src[(int64_t)e * a.din_es] : make_double2(0.0, 0.0);
+  }
+}
+
+// Fused axis-0 column kernel.  blockIdx.x: tile of LPC lines, blockIdx.y: item.
+template <int L, int IN, int OUT, bool HALF>
+__global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const ColArgs a) {
+  using LN = Line<L>;
+  constexpr int LPC = ColCfg<L>::LPC;
+  extern __shared__ double2 smem[];
+  const int line = threadIdx.x % LPC;
+  const int t = threadIdx.x / LPC;
+  const int64_t l = (int64_t)blockIdx.x * LPC + line;
+  const bool valid = l < a.nlines;
+  const int64_t item = blockIdx.y;
+  double2* sm = smem + line * LN::SMEM;
+
+  double2 v[LN::EPT];
+  if constexpr (OUT == OUT_COMPS) {
+    if constexpr (IN == IN_SPARSE) load_sparse<LN, LPC, HALF>(v, a, t, l, item, 0, valid);
+    else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
+    fft_line<LN, false, HALF>(v, t, sm, a.tw, a.lmax);
+#pragma unroll 1
+    for (int j = 0; j < a.n_comp; ++j) {
+      double2 y[LN::EPT];
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kmul(v[r], a.ks[j], l, LN::out_idx(t, r), LN::M) : v[r];
+      fft_line<LN, true>(y, t, sm, a.tw, a.lmax);
+      double2* dst = a.out[j] + item * a.out_item + l;
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) {
+        if (LN::L > 0 && LN::upper_in(r)) continue;
+        const int n = LN::in_idx(t, r);
+        if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = y[r];
+      }
+    }
+  } else if constexpr (OUT == OUT_SUM) {
+    double2 y[LN::EPT];
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) y[r] = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int i = 0; i < a.n_in; ++i) {
+      if constexpr (IN == IN_SPARSE) load_sparse<LN, LPC, HALF>(v, a, t, l, item, i, valid);
+      else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+      fft_line<LN, false, HALF>(v, t, sm, a.tw, a.lmax);
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r)
+        if (valid) y[r] = cadd(y[r], kmul(v[r], a.ks[i], l, LN::out_idx(t, r), LN::M));
+    }
+    fft_line<LN, true>(y, t, sm, a.tw, a.lmax);
+    double2* dst = a.out[0] + item * a.out_item + l;
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) {
+      if (LN::L > 0 && LN::upper_in(r)) continue;
+      const int n = LN::in_idx(t, r);
+      if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = y[r];
+    }
+  } else {  // OUT_SPECTRUM
+#pragma unroll 1
+    for (int i = 0; i < a.n_in; ++i) {
+      if constexpr (IN == IN_SPARSE) load_sparse<LN, LPC, HALF>(v, a, t, l, item, i, valid);
+      else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+      fft_line<LN, false, HALF>(v, t, sm, a.tw, a.lmax);
+      if (!valid) continue;
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) {
+        const int k0 = LN::out_idx(t, r);
+        if (a.spec_mode == SPEC_COMPLEX) {
+          a.out[i][item * a.out_item + (int64_t)k0 * a.out_es + l] = v[r];
+        } else if (a.spec_mode == SPEC_COMPLEX_T) {
+          a.out[i][(int64_t)k0 * a.spec_ld + l] = v[r];
+        } else if (k0 <= (LN::M >> 1)) {
+          a.spec_re[i][(int64_t)k0 * a.spec_ld + l] = (a.spec_mode == SPEC_REAL_T) ? v[r].x : v[r].y;
+        }
+      }
+    }
+  }
+}
+
+// Strided batched c2c lines (3D axis 1, both directions).  Line l of component
+// blockIdx.y: base = (l / inner) * outer_stride + (l % inner); element stride es.
+struct LinesArgs {
+  const double2* in[MAXC];
+  double2* out[MAXC];
+  int64_t nlines, inner, outer_in, outer_out, es_in, es_out;
+  int n_valid, n_out;
+  double scale;
+  const double2* tw;
+  int lmax;
+};
+
+template <int L, bool INV, bool HALF>
+__global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const LinesArgs a) {
+  using LN = Line<L>;
+  constexpr int LPC = ColCfg<L>::LPC;
+  extern __shared__ double2 smem[];
+  const int line = threadIdx.x % LPC;
+  const int t = threadIdx.x / LPC;
+  const int64_t l = (int64_t)blockIdx.x * LPC + line;
+  const bool valid = l < a.nlines;
+  const int c = blockIdx.y;
+  double2* sm = smem + line * LN::SMEM;
+  const int64_t o = valid ? l / a.inner : 0, q = valid ? l % a.inner : 0;
+  const double2* src = a.in[c] + o * a.outer_in + q;
+  double2* dst = a.out[c] + o * a.outer_out + q;
+  double2 v[LN::EPT];
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
+    const int e = INV ? LN::out_idx(t, r) : LN::in_idx(t, r);  // inverse input layout = forward output layout
+    v[r] = (valid && e < a.n_valid) ? src[(int64_t)e * a.es_in] : make_double2(0.0, 0.0);
+  }
+  fft_line<LN, INV, HALF>(v, t, sm, a.tw, a.lmax);
+  if (!valid) return;
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    const int n = INV ? LN::in_idx(t, r) : LN::out_idx(t, r);
+    if (n < a.n_out) {
+      double2 x = v[r];
+      if (a.scale != 1.0) { x.x *= a.scale; x.y *= a.scale; }
+      dst[(int64_t)n * a.es_out] = x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel sample generation (the reference's sampled kernels, R/distance.py:33-37,
+// R/derivatives.py:35-57,139-153, R/sign.py:97-105) on the wrap-around lattice.
+
+enum KType {
+  KT_EXP = 0,
+  KT_GRAD0 = 1, KT_GRAD1 = 2, KT_GRAD2 = 3,   // (o_a/|o|) * exp
+  KT_HXX = 4, KT_HYY = 5, KT_HXY = 6,          // Eq. 40-42 factors * exp (2D)
+  KT_RAT2_0 = 7, KT_RAT2_1 = 8,                // o_a/|o|^2 (2D winding)
+  KT_RAT3_0 = 9, KT_RAT3_1 = 10, KT_RAT3_2 = 11,  // o_a/|o|^3 (3D degree)
+  KT_FIELD = 12,                               // dense user samples (host-provided)
+};
+
+struct GenArgs {
+  int D;            // internal dimension (2 or 3)
+  int c[3];         // grid counts (internal axes)
+  int M[3];         // padded lengths
+  int ref_axis0;    // first internal axis that is a reference axis (1 for 1-D grids)
+  double h, tau, inv_tau, sign;
+  int ktype;
+  const double* field;   // KT_FIELD: samples; fshape/fstride describe it
+  int64_t fcenter[3], fstride[3];
+  int field_is_grid;     // 1: field is a grid array (no wrap, rows [0,c)); 0: centred kernel
+};
+
+// signed offset of padded index j on an axis with count c and length M, or
+// INT_MIN when the index lies outside the kernel support [-(c-1), c-1].
+__device__ __forceinline__ int wrap_offset(int j, int c, int M) {
+  if (j < c) return j;
+  if (j > M - c) return j - M;
+  return -0x40000000;
+}
+
+__device__ __forceinline__ double sample_kernel(const GenArgs& g, int o0, int o1, int o2) {
+  const double h = g.h;
+  // offsets of the reference axes (internal axis 0 is a dummy for 1-D grids)
+  const double m0 = h * (double)o0, m1 = h * (double)o1, m2 = h * (double)o2;
+  const bool centre = (o0 == 0 && o1 == 0 && o2 == 0);
+  if (g.ktype == KT_EXP || (g.ktype >= KT_GRAD0 && g.ktype <= KT_HXY)) {
+    const long long r2i = (long long)o0 * o0 + (long long)o1 * o1 + (long long)o2 * o2;
+    const double base = exp(-(h * sqrt((double)r2i)) / g.tau);
+    if (g.ktype == KT_EXP) return base;
+    // DirectionalKernels: r = sqrt(sum of squared float offsets), 0 at the centre
+    double r;
+    if (g.D == 3) r = sqrt((m0 * m0 + m1 * m1) + m2 * m2);
+    else if (g.ref_axis0 == 1) r = sqrt(m1 * m1);
+    else r = sqrt(m0 * m0 + m1 * m1);
+    if (centre) return 0.0 * base;
+    const double ir = 1.0 / r;
+    double f;
+    if (g.ktype <= KT_GRAD2) {
+      const int a = g.ktype - KT_GRAD0 + g.ref_axis0;
+      const double m = (a == 0) ? m0 : (a == 1 ? m1 : m2);
+      f = m / r;
+    } else {
+      const double fc = m0 / r, fs = m1 / r, it = g.inv_tau;
+      if (g.ktype == KT_HXX) f = ((-it) * fc) * fc + (fs * fs) * ir;
+      else if (g.ktype == KT_HYY) f = ((-it) * fs) * fs + (fc * fc) * ir;
+      else f = ((-(it + ir)) * fc) * fs;
+    }
+    return f * base;
+  }
+  // ratio kernels (sign): numerator / r^p with r from the float offsets
+  double r = (g.D == 3) ? sqrt((m0 * m0 + m1 * m1) + m2 * m2) : sqrt(m0 * m0 + m1 * m1);
+  if (centre) return 0.0;
+  double num;
+  int p;
+  if (g.ktype <= KT_RAT2_1) { num = (g.ktype == KT_RAT2_0) ? m0 : m1; p = 2; }
+  else { const int a = g.ktype - KT_RAT3_0; num = (a == 0) ? m0 : (a == 1 ? m1 : m2); p = 3; }
+  const double den = (p == 2) ? r * r : pow(r, 3.0);
+  return g.sign * (num / den);
+}
+
+// Real sample x[j] of padded row `row` (all non-last padded indices flattened).
+__device__ __forceinline__ double gen_value(const GenArgs& g, int64_t row, int j) {
+  const int D = g.D;
+  int jj[3];
+  if (D == 3) { jj[0] = (int)(row / g.M[1]); jj[1] = (int)(row % g.M[1]); jj[2] = j; }
+  else { jj[0] = (int)row; jj[1] = j; jj[2] = 0; }
+  if (g.ktype == KT_FIELD) {
+    if (g.field_is_grid) {
+      int64_t off = 0;
+      for (int a = 0; a < D; ++a) {
+        if (jj[a] >= g.c[a]) return 0.0;
+        off += (int64_t)jj[a] * g.fstride[a];
+      }
+      return g.field[off];
+    }
+    int64_t off = 0;
+    for (int a = 0; a < D; ++a) {
+      const int o = wrap_offset(jj[a], g.c[a], g.M[a]);
+      if (o == -0x40000000) return 0.0;
+      off += (int64_t)(o + g.fcenter[a]) * g.fstride[a];
+    }
+    return g.field[off];
+  }
+  int o[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) {
+    const int oa = wrap_offset(jj[a], g.c[a], g.M[a]);
+    if (oa == -0x40000000) return 0.0;
+    o[a] = oa;
+  }
+  return (D == 3) ? sample_kernel(g, o[0], o[1], o[2]) : sample_kernel(g, o[0], o[1], 0);
+}
+
+// r2c of padded real rows of length 2*MH: out[row * out_rs + k], k in [0, MH].
+template <int LH>
+__global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const GenArgs g, int64_t nrows,
+                                                                 double2* out, int64_t out_rs,
+                                                                 const double2* tw, int lmax) {
+  using LN = Line<LH>;
+  constexpr int LPC = RowCfg<LH>::LPC;
+  constexpr int MH = LN::M;
+  extern __shared__ double2 smem[];
+  const int line = threadIdx.x / LN::TPL;
+  const int t = threadIdx.x % LN::TPL;
+  const int64_t row = (int64_t)blockIdx.x * LPC + line;
+  const bool valid = row < nrows;
+  double2* sm = smem + line * LN::SMEM;
+  double2 v[LN::EPT];
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    const int m = LN::in_idx(t, r);
+    v[r] = valid ? make_double2(gen_value(g, row, 2 * m), gen_value(g, row, 2 * m + 1)) : make_double2(0.0, 0.0);
+  }
+  fft_line<LN, false>(v, t, sm, tw, lmax);
+  // natural-order spectrum Z into shared memory, then split into X[k], k in [0, MH]
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) sm[spad(LN::out_idx(t, r))] = v[r];
+  __syncthreads();
+  if (!valid) return;
+  const int sh = lmax - (LH + 1);
+  for (int k = t; k <= MH; k += LN::TPL) {
+    const double2 zk = sm[spad(k & (MH - 1))];
+    const double2 zc = sm[spad((MH - k) & (MH - 1))];
+    const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y - zc.y));   // (Z[k] + conj Z[-k]) / 2
+    const double2 d = make_double2(0.5 * (zk.y + zc.y), -0.5 * (zk.x - zc.x));  // (Z[k] - conj Z[-k]) / (2i)
+    const double2 w = __ldg(tw + ((int64_t)k << sh));                          // W_M^k (k = MH -> -1)
+    out[row * out_rs + k] = cadd(e, cmul(d, w));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row pass: c2r along the last axis fused with the epilogue.
+
+struct RowArgs {
+  int64_t rows;        // rows per item
+  int n_out;           // grid count along the last axis
+  int64_t rows_a, stride_a, stride_b, comp_item;  // row -> (row / rows_a)*stride_a + (row % rows_a)*stride_b
+  const double2* comp[MAXC];
+  int n_comp;
+  int c_phi, c_grad, ngrad, c_hess, c_sign, sign_mode, n_raw;  // component slots (-1 absent)
+  double scale, tau, inv_tau;
+  double* S;
+  double* grad[3];
+  double* hess[3];
+  double* mu;
+  uint8_t* mask;
+  uint8_t* uf;
+  double* phi_out;
+  double* raw[MAXC];
+  int64_t N;
+  unsigned long long* uf_count;
+  const double2* tw;
+  int lmax;
+};
+
+template <class LN>
+__device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* __restrict__ X, int t,
+                                         double2* sm, const double2* __restrict__ tw, int lmax, bool valid) {
+  constexpr int MH = LN::M;
+  const int sh = lmax - (LN::L + 1);
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    const int k = LN::out_idx(t, r);
+    if (valid) {
+      const double2 xa = X[k];
+      const double2 xb = X[MH - k];  // conj taken below
+      const double2 e = make_double2(xa.x + xb.x, xa.y - xb.y);   // X[k] + conj X[MH-k]
+      const double2 d = make_double2(xa.x - xb.x, xa.y + xb.y);   // X[k] - conj X[MH-k]
+      const double2 o = cmulc(d, __ldg(tw + ((int64_t)k << sh))); // * W_M^{-k}
+      z[r] = make_double2(e.x - o.y, e.y + o.x);                  // e + i*o
+    } else {
+      z[r] = make_double2(0.0, 0.0);
+    }
+  }
+  fft_line<LN, true>(z, t, sm, tw, lmax);
+}
+
+template <int LH>
+__global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const RowArgs a) {
+  using LN = Line<LH>;
+  constexpr int LPC = RowCfg<LH>::LPC;
+  constexpr int E = LN::EPT;
+  extern __shared__ double2 smem[];
+  const int line = threadIdx.x / LN::TPL;
+  const int t = threadIdx.x % LN::TPL;
+  const int64_t row = (int64_t)blockIdx.x * LPC + line;
+  const bool valid = row < a.rows;
+  const int64_t item = blockIdx.y;
+  double2* sm = smem + line * LN::SMEM;
+  const int64_t roff = item * a.comp_item + (valid ? (row / a.rows_a) * a.stride_a + (row % a.rows_a) * a.stride_b : 0);
+  const int64_t obase = item * a.N + row * a.n_out;
+  const bool even = (a.n_out & 1) == 0;
+
+  auto put = [&](double* dst, int r, double x0, double x1) {
+    const int n = 2 * LN::in_idx(t, r);
+    if (!valid || n >= a.n_out) return;
+    if (even) *reinterpret_cast<double2*>(dst + obase + n) = make_double2(x0, x1);
+    else { dst[obase + n] = x0; if (n + 1 < a.n_out) dst[obase + n + 1] = x1; }
+  };
+  auto putb = [&](uint8_t* dst, int r, uint8_t x0, uint8_t x1) {
+    const int n = 2 * LN::in_idx(t, r);
+    if (!valid || n >= a.n_out) return;
+    dst[obase + n] = x0;
+    if (n + 1 < a.n_out) dst[obase + n + 1] = x1;
+  };
+  auto active = [&](int r) { return !(LN::L > 0 && LN::upper_in(r)); };
+
+  double2 phi[E], sg[3][E];
+  double2 z[E];
+  unsigned cnt = 0;
+  if (a.c_phi >= 0) {
+    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, sm, a.tw, a.lmax, valid);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if (!active(r)) continue;
+      phi[r] = make_double2(z[r].x * a.scale, z[r].y * a.scale);
+      const int n = 2 * LN::in_idx(t, r);
+      if (valid && n < a.n_out) {
+        cnt += (phi[r].x <= 0.0);
+        if (n + 1 < a.n_out) cnt += (phi[r].y <= 0.0);
+      }
+      if (a.phi_out) put(a.phi_out, r, phi[r].x, phi[r].y);
+      if (a.S) {
+        const double s0 = phi[r].x > 0.0 ? (-a.tau) * log(phi[r].x) : __longlong_as_double(0x7ff8000000000000LL);
+        const double s1 = phi[r].y > 0.0 ? (-a.tau) * log(phi[r].y) : __longlong_as_double(0x7ff8000000000000LL);
+        put(a.S, r, s0, s1);
+      }
+      if (a.uf) putb(a.uf, r, phi[r].x <= 0.0, phi[r].y <= 0.0);
+    }
+  }
+  if (a.c_grad >= 0) {
+#pragma unroll 1
+    for (int d = 0; d < a.ngrad; ++d) {
+      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, sm, a.tw, a.lmax, valid);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        if (!active(r)) continue;
+        const double2 q = make_double2((z[r].x * a.scale) / phi[r].x, (z[r].y * a.scale) / phi[r].y);
+        if (d == 0) sg[0][r] = q; else if (d == 1) sg[1][r] = q; else sg[2][r] = q;
+        if (a.grad[d]) put(a.grad[d], r, q.x, q.y);
+      }
+    }
+  }
+  if (a.c_hess >= 0) {
+#pragma unroll 1
+    for (int d = 0; d < 3; ++d) {
+      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, sm, a.tw, a.lmax, valid);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        if (!active(r)) continue;
+        const double2 tq = make_double2((z[r].x * a.scale) / phi[r].x, (z[r].y * a.scale) / phi[r].y);
+        // xx: tq + (1/tau) sx sx, yy: tq + (1/tau) sy sy, xy: tq + (1/tau) sx sy (R/derivatives.py:102-106)
+        const double2 u = (d == 1) ? sg[1][r] : sg[0][r];
+        const double2 pw = (d == 0) ? sg[0][r] : sg[1][r];
+        const double2 hv = make_double2(tq.x + (a.inv_tau * u.x) * pw.x, tq.y + (a.inv_tau * u.y) * pw.y);
+        put(a.hess[d], r, hv.x, hv.y);
+      }
+    }
+  }
+  if (a.c_sign >= 0) {
+    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, sm, a.tw, a.lmax, valid);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if (!active(r)) continue;
+      const double u0 = z[r].x * a.scale, u1 = z[r].y * a.scale;
+      double m0, m1;
+      uint8_t b0, b1;
+      if (a.sign_mode == 1) {
+        m0 = u0 / 6.283185307179586;
+        m1 = u1 / 6.283185307179586;
+        b0 = rint(m0) > 0.0; b1 = rint(m1) > 0.0;
+      } else {
+        m0 = -u0 / 12.566370614359172;
+        m1 = -u1 / 12.566370614359172;
+        b0 = rint(m0) >= 1.0; b1 = rint(m1) >= 1.0;
+      }
+      if (a.mu) put(a.mu, r, m0, m1);
+      if (a.mask) putb(a.mask, r, b0, b1);
+    }
+  }
+#pragma unroll 1
+  for (int j = 0; j < a.n_raw; ++j) {
+    c2r_line<LN>(z, a.comp[j] + roff, t, sm, a.tw, a.lmax, valid);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      if (!active(r)) continue;
+      put(a.raw[j], r, z[r].x * a.scale, z[r].y * a.scale);
+    }
+  }
+  if (a.uf_count) {
+    const unsigned tot = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.uf_count, (unsigned long long)tot);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Node-list preparation: validation + per-row CSR, deterministic.
+
+static __global__ void prep_nodes_kernel(const int64_t* __restrict__ nodes, const int64_t* __restrict__ item_off,
+                                  int64_t clast, int64_t rows_per_item, int64_t N,
+                                  int64_t* __restrict__ rowid, int32_t* __restrict__ cols, int* err) {
+  const int64_t item = blockIdx.y;
+  const int64_t p0 = item_off[item], p1 = item_off[item + 1];
+  for (int64_t p = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nd = nodes[p];
+    if (nd < 0 || nd >= N || (p > p0 && nodes[p - 1] >= nd)) atomicExch(err, 1);
+    const int64_t ndc = nd < 0 ? 0 : (nd >= N ? N - 1 : nd);
+    rowid[p] = item * rows_per_item + ndc / clast;
+    cols[p] = (int32_t)(ndc % clast);
+  }
+}
+
+static __global__ void rowptr_kernel(const int64_t* __restrict__ rowid, int64_t K, int64_t nrows, int64_t* __restrict__ rowptr) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r > nrows) return;
+  int64_t lo = 0, hi = K;  // first p with rowid[p] >= r
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rowid[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  rowptr[r] = lo;
+}
+
+}  // namespace eik

@@ -1,0 +1,25 @@
+#include "launch.cuh"
+
+template <int L, int IN, int OUT, bool HALF>
+int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
+  using C = ColCfg<L>;
+  auto k = col_kernel<L, IN, OUT, HALF>;
+  CK(prep_kernel_attr(k, C::SMEM_BYTES));
+  const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
+  if (tiles <= 0 || items <= 0) return EIK_OK;
+  if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
+  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);
+  CK(cudaGetLastError());
+  return EIK_OK;
+}
+
+template <int IN, int OUT, bool HALF>
+int launch_col(int L, const ColArgs& a, int64_t items, cudaStream_t st) {
+#define EIK_COL(Lc) return launch_col_t<Lc, IN, OUT, HALF>(a, items, st)
+  EIK_SWITCH_L(L, EIK_COL);
+#undef EIK_COL
+  return EIK_OK;
+}
+
+
+template int launch_col<IN_DENSE, OUT_SPECTRUM, false>(int, const ColArgs&, int64_t, cudaStream_t);

@@ -1,0 +1,103 @@
+"""Unsigned distance S = -tau log(exp(-|x|/tau) * delta_Y) on the GPU.
+
+Drop-in for the FFT entry points of R/distance.py (kernel_exp 22-47,
+impulse_field 50-60, phi_fft 63-86, s_from_phi 89-111, s_fft 114-122).
+The arithmetic runs in libeikfld_b200 (one fused pipeline: impulse DFT from
+the node list, cached kernel spectrum, pruned r2c/c2r passes, -tau log phi
+epilogue with underflow detection).  Same names, argument meaning and errors.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .errors import PrecisionError, ValidationError
+from .grid import ScalarField
+from .precision import log_bound, require_native
+
+_UNDERFLOW_MSG = (
+    "{what} has non-positive entries after convolution; increase the precision bits "
+    "(e.g. --precision big:512) or raise tau"
+)
+
+
+def distinct_nodes(ps, grid) -> np.ndarray:
+    """Sorted distinct snapped nodes with the reference's bounds check (R/distance.py:55-58)."""
+    nodes = np.unique(np.asarray(ps.snapped_indices, dtype=np.int64))
+    if nodes.size == 0:
+        raise ValidationError("point-set must contain at least one point")
+    if nodes[0] < 0 or nodes[-1] >= grid.num_nodes:
+        raise ValidationError("snapped index out of grid bounds")
+    return nodes
+
+
+def _check_grid(grid):
+    if not 1 <= len(grid.counts) <= 3:
+        raise ValidationError("dimension must be 1, 2 or 3")
+
+
+def kernel_exp(grid, cfg):
+    """Sampled exp(-|offset|/tau) on [-(c-1), c-1]^D, as R/distance.py:22-47.
+
+    Host-side sampling kept for API compatibility (tests, FftConvolver users);
+    the GPU pipeline generates these samples on the device and never reads this.
+    """
+    from .convolution import KernelField
+
+    tau = require_native(cfg)
+    mesh = np.meshgrid(*[np.arange(-(c - 1), c) for c in grid.counts], indexing="ij")
+    r2 = sum(m.astype(np.int64) ** 2 for m in mesh)
+    return KernelField(grid.spacing, np.exp(-(grid.spacing * np.sqrt(r2.astype(np.float64))) / tau))
+
+
+def impulse_field(ps, grid) -> ScalarField:
+    """Unit impulses at the distinct snapped nodes (R/distance.py:50-60)."""
+    vals = np.zeros(grid.num_nodes, dtype=np.float64)
+    vals[distinct_nodes(ps, grid)] = 1.0
+    return ScalarField(grid, vals)
+
+
+def _run_phi_family(ps, grid, cfg, *, want_s: bool, what: str):
+    tau = require_native(cfg)
+    _check_grid(grid)
+    nodes = distinct_nodes(ps, grid)
+    plan = _native.get_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S)
+    out = np.empty(grid.num_nodes, dtype=np.float64)
+    kw = {"S": out} if want_s else {"phi": out}
+    try:
+        plan.run(nodes, check_underflow=True, **kw)
+    except PrecisionError:
+        raise PrecisionError(_UNDERFLOW_MSG.format(what=what)) from None
+    return out
+
+
+def phi_fft(ps, grid, cfg, convolver=None, kernel_hat=None) -> ScalarField:
+    """phi = exp(-|x|/tau) * delta_Y on the grid; PrecisionError if any phi <= 0.
+
+    `convolver`/`kernel_hat` are accepted for signature compatibility; kernel
+    spectra are always reused through the plan cache (the reference's reuse hook).
+    """
+    return ScalarField(grid, _run_phi_family(ps, grid, cfg, want_s=False, what="phi"))
+
+
+def s_from_phi(phi: ScalarField, cfg) -> ScalarField:
+    """S = -tau log(phi) for a given phi field (R/distance.py:89-111)."""
+    tau = require_native(cfg)
+    vals = np.asarray(phi.values, dtype=np.float64)
+    if (vals <= 0).any():
+        raise PrecisionError("phi <= 0: native64 underflow; rerun with --precision big:<bits>")
+    return ScalarField(phi.grid, -tau * np.log(vals))
+
+
+def s_fft(ps, grid, cfg, convolver=None, kernel_hat=None) -> ScalarField:
+    """Composed pipeline (R/distance.py:114-122), fused on the device."""
+    return ScalarField(grid, _run_phi_family(ps, grid, cfg, want_s=True, what="phi"))
+
+
+def error_bound(cfg, k: int) -> float:
+    return log_bound(cfg.tau, k)
+
+
+def clamp_nonnegative(field: ScalarField) -> ScalarField:
+    return ScalarField(field.grid, np.maximum(field.values, 0.0), field.flagged_nodes)

@@ -1,0 +1,138 @@
+"""Winding number (2-D) and topological degree (3-D) sign fields on the GPU.
+
+Drop-in for R/sign.py (WINDING_2D/DEGREE_3D 24-25, TangentData 34-57,
+FluxData 60-86, winding_field 108-132, degree_field 135-163, classify
+166-198, signed_distance 201-208).  The weighted impulses are accumulated per
+node on the host in exactly the order np.add.at uses (so the weights are
+bit-identical to the reference's), then the device runs the same spectral
+pipeline as the distance: impulse DFTs straight from the (node, weight)
+lists, multiply by the cached x/r^2 (2-D) or x/r^3 (3-D) kernel spectra,
+summed, one inverse, mu = h/(2 pi) or -h/(4 pi) in the fused epilogue.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ValidationError
+from .grid import ScalarField, snap_points
+from .precision import require_native
+
+WINDING_2D = "winding2d"
+DEGREE_3D = "degree3d"
+
+
+def _accumulate(idx: np.ndarray, weights: np.ndarray):
+    """Distinct nodes and per-node sums in np.add.at order (sequential, from 0.0)."""
+    nodes, inv = np.unique(idx, return_inverse=True)
+    acc = np.zeros((weights.shape[1], nodes.size))
+    for a in range(weights.shape[1]):
+        np.add.at(acc[a], inv, weights[:, a])
+    return nodes, acc
+
+
+@dataclass(frozen=True)
+class TangentData:
+    """Snapped chord tangents per vertex and their per-node sums (R/sign.py:34-57)."""
+
+    vertex_nodes: np.ndarray
+    tangents: np.ndarray
+    nodes: np.ndarray
+    weights: np.ndarray  # (2, len(nodes))
+
+    @classmethod
+    def build(cls, curve, grid) -> "TangentData":
+        if len(grid.counts) != 2:
+            raise ValidationError("winding numbers need a 2D grid")
+        ps = snap_points(curve.vertices, grid)
+        snapped = grid.coords_of_flat(ps.snapped_indices)
+        tangents = np.roll(snapped, -1, axis=0) - snapped
+        nodes, w = _accumulate(ps.snapped_indices, tangents)
+        return cls(vertex_nodes=nodes, tangents=tangents, nodes=nodes, weights=w)
+
+
+@dataclass(frozen=True)
+class FluxData:
+    """Area-weighted normals at snapped triangle centres (R/sign.py:60-86)."""
+
+    center_nodes: np.ndarray
+    nodes: np.ndarray
+    weights: np.ndarray  # (3, len(nodes))
+
+    @classmethod
+    def build(cls, surface, grid) -> "FluxData":
+        if len(grid.counts) != 3:
+            raise ValidationError("topological degree needs a 3D grid")
+        ps = snap_points(surface.centers, grid)
+        e1 = surface.triangles[:, 1] - surface.triangles[:, 0]
+        e2 = surface.triangles[:, 2] - surface.triangles[:, 0]
+        areas = 0.5 * np.linalg.norm(np.cross(e1, e2), axis=1)
+        nodes, w = _accumulate(ps.snapped_indices, surface.normals * areas[:, None])
+        return cls(center_nodes=nodes, nodes=nodes, weights=w)
+
+
+def _sign_run(grid, tau, field_bit, nodes, weights, want_mask=False):
+    plan = _native.get_plan(grid, tau, field_bit)
+    mu = np.empty(grid.num_nodes)
+    mask = np.empty(grid.num_nodes, dtype=np.uint8) if want_mask else None
+    plan.run(sign_nodes=np.ascontiguousarray(nodes, dtype=np.int64),
+             sign_weights=np.ascontiguousarray(weights, dtype=np.float64), mu=mu, mask=mask)
+    return mu, mask
+
+
+def winding_field(curve, grid, cfg) -> ScalarField:
+    """Winding number at every node, counter-clockwise positive; vertex nodes flagged."""
+    tau = require_native(cfg)
+    data = TangentData.build(curve, grid)
+    mu, _ = _sign_run(grid, tau, _native.FIELD_WINDING, data.nodes, data.weights)
+    return ScalarField(grid, mu, flagged_nodes=data.vertex_nodes)
+
+
+def degree_field(surface, grid, cfg) -> ScalarField:
+    """Normalized flux (topological degree); triangle-centre nodes flagged."""
+    tau = require_native(cfg)
+    data = FluxData.build(surface, grid)
+    mu, _ = _sign_run(grid, tau, _native.FIELD_DEGREE, data.nodes, data.weights)
+    return ScalarField(grid, mu, flagged_nodes=data.center_nodes)
+
+
+def classify(mu: ScalarField, mode: str, threshold: float | None = None) -> ScalarField:
+    """Interior mask: rint(mu) > 0 (2-D) / >= 1 (3-D) or mu >= threshold.
+
+    Flagged nodes take the value of their nearest unflagged node (grid-index
+    metric, scipy's EDT tie-breaking) as R/sign.py:166-198 does.  This fill
+    runs on the host (SURVEY.md §8(f) rank 3 lists the GPU version as next).
+    """
+    from scipy import ndimage
+
+    if mode not in (WINDING_2D, DEGREE_3D):
+        raise ValidationError(f"unknown classification mode {mode!r}")
+    vals = np.asarray(mu.values, dtype=np.float64).copy()
+    if mu.flagged_nodes is not None and mu.flagged_nodes.size:
+        fl = np.zeros(mu.grid.num_nodes, dtype=bool)
+        fl[mu.flagged_nodes] = True
+        if fl.all():
+            raise ValidationError("every node is flagged; cannot classify")
+        _, near = ndimage.distance_transform_edt(fl.reshape(mu.grid.shape), return_indices=True)
+        fill = vals.reshape(mu.grid.shape)[tuple(near)]
+        vals = np.where(fl, fill.reshape(-1), vals)
+    if threshold is not None:
+        inside = vals >= threshold
+    elif mode == WINDING_2D:
+        inside = np.rint(vals) > 0
+    else:
+        inside = np.rint(vals) >= 1
+    return ScalarField(mu.grid, inside.astype(np.float64), flagged_nodes=mu.flagged_nodes)
+
+
+def signed_distance(s: ScalarField, mask: ScalarField) -> ScalarField:
+    if mask.grid != s.grid:
+        raise ValidationError("mask and distance field grids differ")
+    return ScalarField(s.grid, np.where(mask.values > 0.5, s.values, -s.values), s.flagged_nodes)
+
+
+_TWO_PI = 2.0 * math.pi
