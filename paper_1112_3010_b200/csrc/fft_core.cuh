@@ -67,40 +67,61 @@ __device__ __forceinline__ double2 w16(double2 a, int q) {
 }
 
 __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
-__host__ __device__ constexpr int bitrev(int n, int bits) {
-  return bits == 0 ? 0 : (((n & 1) << (bits - 1)) | bitrev(n >> 1, bits - 1));
+
+// Compile-time bit reversal (a template constant, so register indices stay static).
+template <int N, int BITS>
+struct BitRev {
+  static constexpr int value = BITS == 0 ? 0 : (((N & 1) << (BITS - 1)) | BitRev<(N >> 1), (BITS > 0 ? BITS - 1 : 0)>::value);
+};
+template <int N>
+struct BitRev<N, 0> {
+  static constexpr int value = 0;
+};
+
+template <int R, int N, bool HALF_IN>
+__device__ __forceinline__ void perm_load(double2* x, const double2* a) {
+  if constexpr (N < R) {
+    if constexpr (!(HALF_IN && (N & 1))) x[N] = a[BitRev<N, ilog2c(R)>::value];
+    perm_load<R, N + 1, HALF_IN>(x, a);
+  }
+}
+
+// One radix-2 level of length LEN over the R registers (compile-time indices).
+template <int R, int LEN, int S, int K, bool INV, bool HALF_IN>
+__device__ __forceinline__ void bfly_level(double2* x) {
+  if constexpr (S < R) {
+    if constexpr (K < LEN / 2) {
+      if constexpr (HALF_IN && LEN == 2) {
+        x[S + 1] = x[S];
+      } else {
+        const double2 u = x[S + K];
+        const double2 w = w16<INV>(x[S + K + LEN / 2], K * (16 / LEN));
+        x[S + K] = cadd(u, w);
+        x[S + K + LEN / 2] = csub(u, w);
+      }
+      bfly_level<R, LEN, S, K + 1, INV, HALF_IN>(x);
+    } else {
+      bfly_level<R, LEN, S + LEN, 0, INV, HALF_IN>(x);
+    }
+  }
+}
+
+template <int R, int LEN, bool INV, bool HALF_IN>
+__device__ __forceinline__ void bfly_levels(double2* x) {
+  if constexpr (LEN <= R) {
+    bfly_level<R, LEN, 0, 0, INV, HALF_IN>(x);
+    bfly_levels<R, LEN * 2, INV, HALF_IN>(x);
+  }
 }
 
 // In-register R-point DFT (natural order in/out), radix-2 DIT, R <= 16.
 // HALF_IN: a[R/2..R) are known zero (not read).
 template <int R, bool INV, bool HALF_IN>
 __device__ __forceinline__ void dft(double2* a) {
-  if constexpr (R == 1) {
-    return;
-  } else {
-    constexpr int B = ilog2c(R);
+  if constexpr (R > 1) {
     double2 x[R];
-#pragma unroll
-    for (int n = 0; n < R; ++n) {
-      if (!(HALF_IN && (n & 1))) x[n] = a[bitrev(n, B)];
-    }
-#pragma unroll
-    for (int len = 2; len <= R; len <<= 1) {
-#pragma unroll
-      for (int s = 0; s < R; s += len) {
-#pragma unroll
-        for (int k = 0; k < len / 2; ++k) {
-          if (HALF_IN && len == 2) {
-            x[s + 1] = x[s];
-          } else {
-            double2 u = x[s + k];
-            double2 w = w16<INV>(x[s + k + len / 2], k * (16 / len));
-            x[s + k] = cadd(u, w);
-            x[s + k + len / 2] = csub(u, w);
-          }
-        }
-      }
-    }
+    perm_load<R, 0, HALF_IN>(x, a);
+    bfly_levels<R, 2, INV, HALF_IN>(x);
 #pragma unroll
     for (int n = 0; n < R; ++n) a[n] = x[n];
   }

@@ -135,7 +135,7 @@ __device__ __forceinline__ void load_dense(double2 (&v)[LN::EPT], const ColArgs&
 
 // Fused axis-0 column kernel.  blockIdx.x: tile of LPC lines, blockIdx.y: item.
 template <int L, int IN, int OUT, bool HALF>
-__global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const ColArgs a) {
+__global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constant__ ColArgs a) {
   using LN = Line<L>;
   constexpr int LPC = ColCfg<L>::LPC;
   extern __shared__ double2 smem[];
@@ -221,7 +221,7 @@ struct LinesArgs {
 };
 
 template <int L, bool INV, bool HALF>
-__global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const LinesArgs a) {
+__global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_constant__ LinesArgs a) {
   using LN = Line<L>;
   constexpr int LPC = ColCfg<L>::LPC;
   extern __shared__ double2 smem[];
@@ -361,7 +361,7 @@ __device__ __forceinline__ double gen_value(const GenArgs& g, int64_t row, int j
 
 // r2c of padded real rows of length 2*MH: out[row * out_rs + k], k in [0, MH].
 template <int LH>
-__global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const GenArgs g, int64_t nrows,
+__global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_constant__ GenArgs g, int64_t nrows,
                                                                  double2* out, int64_t out_rs,
                                                                  const double2* tw, int lmax) {
   using LN = Line<LH>;
@@ -444,7 +444,7 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
 }
 
 template <int LH>
-__global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const RowArgs a) {
+__global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_constant__ RowArgs a) {
   using LN = Line<LH>;
   constexpr int LPC = RowCfg<LH>::LPC;
   constexpr int E = LN::EPT;
