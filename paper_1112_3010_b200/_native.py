@@ -127,9 +127,13 @@ class Plan:
         return {n: v for n, v in zip(PASS_NAMES, ms) if v >= 0}
 
     def close(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            lib().eik_plan_destroy(self._h)
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
             self._h = C.c_void_p()
+            try:
+                lib().eik_plan_destroy(h)
+            except Exception:  # interpreter shutdown: the process releases the device anyway
+                pass
 
     __del__ = close
 

@@ -129,18 +129,45 @@ __device__ __forceinline__ void dft(double2* a) {
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 3); }
 
-// Compile-time description of a length-2^L line transform.
-template <int L_>
+// Quarter-wave twiddle table in shared memory: q[k] = W_Q^k = exp(-2 pi i k / Q),
+// k in [0, Q/4), Q = 2^lq.  Any W_Q^j is one table read plus a quadrant rotation,
+// so the table for a 4096-point line is ~19 KB instead of 64 KB.  Stage
+// twiddles are read at power-of-two strides; the multi-level padding tpos()
+// spreads such strides over distinct 16-byte bank groups.
+__device__ __forceinline__ int tpos(int k) { return k + (k >> 3) + (k >> 6) + (k >> 9) + (k >> 12); }
+__host__ __device__ constexpr int tpos_size(int n) { return n + (n >> 3) + (n >> 6) + (n >> 9) + (n >> 12) + 1; }
+
+__device__ __forceinline__ double2 twq_get(const double2* q, int lq, int j) {
+  const int qb = lq - 2;
+  const int quad = (j >> qb) & 3;
+  const double2 w = q[tpos(j & ((1 << qb) - 1))];
+  const double2 r = (quad & 1) ? make_double2(w.y, -w.x) : w;  // * W_Q^{Q/4} = -i
+  return (quad & 2) ? make_double2(-r.x, -r.y) : r;
+}
+
+// Fill the quarter table from the plan's global table W_MAX^j (MAX = 2^lmax); call
+// from every thread of the block, followed by __syncthreads().
+__device__ __forceinline__ void twq_fill(double2* q, int lq, const double2* __restrict__ gtw, int lmax) {
+  const int n = 1 << (lq - 2);
+  for (int k = threadIdx.x; k < n; k += blockDim.x) q[tpos(k)] = __ldg(gtw + ((int64_t)k << (lmax - lq)));
+}
+
+// Compile-time description of a length-2^L line transform with at most E
+// elements (and radix) per thread.
+template <int L_, int E_ = 16>
 struct Line {
   static constexpr int L = L_;
+  static constexpr int E = E_;
+  static constexpr int LE = ilog2c(E_);
   static constexpr int M = 1 << L;
-  static constexpr int EPT = (L <= 4) ? M : 16;
+  static constexpr int EPT = (M <= E) ? M : E;
   static constexpr int TPL = M / EPT;
-  static constexpr int NST = (L == 0) ? 0 : ((L <= 4) ? 1 : (L + 3) / 4);
-  static constexpr int R0 = (L <= 4) ? M : ((L % 4) ? (1 << (L % 4)) : 16);
-  static constexpr int RL = (NST <= 1) ? R0 : 16;
+  static constexpr int NST = (L == 0) ? 0 : ((L <= LE) ? 1 : (L + LE - 1) / LE);
+  static constexpr int R0 = (L <= LE) ? M : ((L % LE) ? (1 << (L % LE)) : E);
+  static constexpr int RL = (NST <= 1) ? R0 : E;
   static constexpr int SMEM = M + (M >> 3) + 1;  // padded double2 slots per line
-  __host__ __device__ static constexpr int frad(int s) { return s == 0 ? R0 : 16; }
+  static constexpr int TWQ = tpos_size((L >= 2) ? (M >> 2) : 1);  // quarter-table slots (own resolution)
+  __host__ __device__ static constexpr int frad(int s) { return s == 0 ? R0 : E; }
   __host__ __device__ static constexpr int rad(bool inv, int s) { return inv ? frad(NST - 1 - s) : frad(s); }
   __host__ __device__ static constexpr int ns(bool inv, int s) { return s == 0 ? 1 : ns(inv, s - 1) * rad(inv, s - 1); }
   // element index held by register i of thread t
@@ -156,10 +183,9 @@ struct Line {
 
 // One Stockham stage S of direction INV, followed (if not last) by the
 // shared-memory exchange into the next stage's register layout.
-// tw: table of W_MAX^j, j in [0, MAX); lmax = log2(MAX).
+// twq: shared quarter table at resolution 2^lq (lq >= L).
 template <class LN, bool INV, int S, bool HALF_IN>
-__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm,
-                                      const double2* __restrict__ tw, int lmax) {
+__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm, const double2* twq, int lq) {
   constexpr int R = LN::rad(INV, S);
   constexpr int NS = LN::ns(INV, S);
   constexpr int G = LN::EPT / R;
@@ -168,10 +194,10 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm,
     const int b = t + g * LN::TPL;
     if constexpr (NS > 1) {
       const int k = b & (NS - 1);
-      const int sh = lmax - ilog2c(NS * R);
+      const int sh = lq - ilog2c(NS * R);
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        const double2 w = __ldg(tw + ((k * r) << sh));
+        const double2 w = twq_get(twq, lq, (k * r) << sh);
         v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
       }
     }
@@ -199,21 +225,19 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm,
 }
 
 template <class LN, bool INV, int S, bool HALF_IN>
-__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, double2* sm,
-                                            const double2* __restrict__ tw, int lmax) {
+__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, double2* sm, const double2* twq, int lq) {
   if constexpr (S < LN::NST) {
-    stage<LN, INV, S, HALF_IN>(v, t, sm, tw, lmax);
-    stages_from<LN, INV, S + 1, HALF_IN>(v, t, sm, tw, lmax);
+    stage<LN, INV, S, HALF_IN>(v, t, sm, twq, lq);
+    stages_from<LN, INV, S + 1, HALF_IN>(v, t, sm, twq, lq);
   }
 }
 
 // Full transform of the line held in v (layouts documented above).
 // HALF_IN (forward only): input elements >= M/2 are zero and their registers are not read.
 template <class LN, bool INV, bool HALF_IN = false>
-__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, double2* sm,
-                                         const double2* __restrict__ tw, int lmax) {
+__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, double2* sm, const double2* twq, int lq) {
   static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
-  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, sm, tw, lmax);
+  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, sm, twq, lq);
 }
 
 }  // namespace eik

@@ -31,21 +31,33 @@ enum { IN_SPARSE = 0, IN_DENSE = 1 };
 enum { OUT_COMPS = 0, OUT_SUM = 1, OUT_SPECTRUM = 2 };
 enum { SPEC_COMPLEX = 0, SPEC_REAL_T = 1, SPEC_IMAG_T = 2, SPEC_COMPLEX_T = 3 };
 
-// Threads per CTA for a column kernel of length 2^L, and lines per CTA.
+// Launch shapes.  Column kernels (col/lines): lines of length 2^L, E elements
+// per thread, NT threads, LPC lines per CTA, then the line buffers and a
+// quarter twiddle table of the line length in dynamic shared memory.  Long
+// lines use E = 8 so the forward result and the per-component product both
+// stay in registers without spilling at 512 threads.
+#ifndef EIK_COL_E_LARGE
+#define EIK_COL_E_LARGE 8
+#endif
+__host__ __device__ constexpr int col_e(int L) { return (L >= 10 && L <= 12) ? EIK_COL_E_LARGE : 16; }
 __host__ __device__ constexpr int col_threads(int L) { return L >= 10 ? 512 : 256; }
 template <int L>
 struct ColCfg {
-  using LN = Line<L>;
+  using LN = Line<L, col_e(L)>;
   static constexpr int NT = (col_threads(L) > LN::TPL) ? col_threads(L) : LN::TPL;
   static constexpr int LPC = NT / LN::TPL;
-  static constexpr size_t SMEM_BYTES = (size_t)LPC * LN::SMEM * sizeof(double2);
+  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ) * sizeof(double2);
 };
-template <int L>
+// Row kernels (c2r / r2c along the contiguous last axis): complex lines of
+// length 2^LH = M_last/2, quarter table at the resolution of M_last.
+__host__ __device__ constexpr int row_e(int LH) { return LH >= 9 ? 8 : 16; }
+template <int LH>
 struct RowCfg {
-  using LN = Line<L>;
+  using LN = Line<LH, row_e(LH)>;
   static constexpr int NT = (LN::TPL >= 128) ? LN::TPL : 128;
   static constexpr int LPC = NT / LN::TPL;
-  static constexpr size_t SMEM_BYTES = (size_t)LPC * LN::SMEM * sizeof(double2);
+  static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
+  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + TWQ) * sizeof(double2);
 };
 
 // Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
@@ -96,22 +108,49 @@ __device__ __forceinline__ double2 kmul(double2 x, const KSpec& k, int64_t l, in
   return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
 }
 
-template <class LN, int LPC, bool HALF>
+// Raw folded kernel spectrum value at (k0, l); the fold sign is applied at use
+// time (kapply) so a prefetch issued one FFT ahead does not stall on the load.
+__device__ __forceinline__ double kload(const KSpec& k, int64_t l, int k0, int M0) {
+  const bool hi = k0 > (M0 >> 1);
+  return __ldg(k.re + (int64_t)(hi ? M0 - k0 : k0) * k.ld + l);
+}
+__device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0) {
+  if (k.odd0 && k0 > (M0 >> 1)) v = -v;
+  return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
+}
+
+// Impulse DFT along the last axis straight from the per-row node lists:
+// v[e] = sum_{p in row e} w_p W_{M_last}^{col_p * l}; each row accumulates its
+// points in list order (bit-reproducible).  Row bounds for all registers are
+// loaded first so their L2 latencies overlap.
+constexpr size_t SPARSE_SMEM = 0;
+template <class LN, bool HALF>
 __device__ __forceinline__ void load_sparse(double2 (&v)[LN::EPT], const ColArgs& a, int t, int64_t l,
-                                            int64_t item, int inp, bool valid) {
+                                            int64_t item, int inp, bool valid, const double2* twq) {
+  // W_{M_last}^{col*l}: from the shared quarter table when M_last <= M0, else global
+  const int llast = a.lmax - a.last_shift;
+  const bool shared_tw = llast <= LN::L && LN::L >= 2;
+  const int up = LN::L - llast;
   const double* __restrict__ w = a.w[inp];
+  const int64_t row0 = item * a.rows_per_item;
+  int64_t lo[LN::EPT], hi[LN::EPT];
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
+    lo[r] = hi[r] = 0;
     if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
     const int e = LN::in_idx(t, r);
-    double2 acc = make_double2(0.0, 0.0);
     if (valid && e < a.n_valid) {
-      const int64_t row = item * a.rows_per_item + e;
-      const int64_t p0 = __ldg(a.rowptr + row), p1 = __ldg(a.rowptr + row + 1);
-      for (int64_t p = p0; p < p1; ++p) {
-        const int col = __ldg(a.cols + p);
-        const int idx = (int)(((int64_t)col * l) & a.last_mask) << a.last_shift;
-        const double2 tw = __ldg(a.tw + idx);
+      lo[r] = __ldg(a.rowptr + row0 + e);
+      hi[r] = __ldg(a.rowptr + row0 + e + 1);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    double2 acc = make_double2(0.0, 0.0);
+    if (!(HALF && LN::L > 0 && LN::upper_in(r))) {
+      for (int64_t p = lo[r]; p < hi[r]; ++p) {
+        const int j = (int)(((int64_t)__ldg(a.cols + p) * l) & a.last_mask);
+        const double2 tw = shared_tw ? twq_get(twq, LN::L, j << up) : __ldg(a.tw + (j << a.last_shift));
         const double wt = w ? __ldg(w + p) : 1.0;
         acc.x = fma(wt, tw.x, acc.x);
         acc.y = fma(wt, tw.y, acc.y);
@@ -136,7 +175,7 @@ __device__ __forceinline__ void load_dense(double2 (&v)[LN::EPT], const ColArgs&
 // Fused axis-0 column kernel.  blockIdx.x: tile of LPC lines, blockIdx.y: item.
 template <int L, int IN, int OUT, bool HALF>
 __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constant__ ColArgs a) {
-  using LN = Line<L>;
+  using LN = typename ColCfg<L>::LN;
   constexpr int LPC = ColCfg<L>::LPC;
   extern __shared__ double2 smem[];
   const int line = threadIdx.x % LPC;
@@ -145,18 +184,36 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   const bool valid = l < a.nlines;
   const int64_t item = blockIdx.y;
   double2* sm = smem + line * LN::SMEM;
+  double2* twq = smem + LPC * LN::SMEM;
+  if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
+  __syncthreads();
 
   double2 v[LN::EPT];
   if constexpr (OUT == OUT_COMPS) {
-    if constexpr (IN == IN_SPARSE) load_sparse<LN, LPC, HALF>(v, a, t, l, item, 0, valid);
+    if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
     else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
-    fft_line<LN, false, HALF>(v, t, sm, a.tw, a.lmax);
+    fft_line<LN, false, HALF>(v, t, sm, twq, L);
+    const bool real_ks = a.ks[0].cplx == nullptr;
+    double kn[LN::EPT];  // next component's kernel spectrum, prefetched
+    if (real_ks && valid) {
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[0], l, LN::out_idx(t, r), LN::M);
+    }
 #pragma unroll 1
     for (int j = 0; j < a.n_comp; ++j) {
       double2 y[LN::EPT];
+      if (real_ks) {
 #pragma unroll
-      for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kmul(v[r], a.ks[j], l, LN::out_idx(t, r), LN::M) : v[r];
-      fft_line<LN, true>(y, t, sm, a.tw, a.lmax);
+        for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M) : v[r];
+        if (j + 1 < a.n_comp && valid) {
+#pragma unroll
+          for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[j + 1], l, LN::out_idx(t, r), LN::M);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kmul(v[r], a.ks[j], l, LN::out_idx(t, r), LN::M) : v[r];
+      }
+      fft_line<LN, true>(y, t, sm, twq, L);
       double2* dst = a.out[j] + item * a.out_item + l;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
@@ -171,14 +228,23 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     for (int r = 0; r < LN::EPT; ++r) y[r] = make_double2(0.0, 0.0);
 #pragma unroll 1
     for (int i = 0; i < a.n_in; ++i) {
-      if constexpr (IN == IN_SPARSE) load_sparse<LN, LPC, HALF>(v, a, t, l, item, i, valid);
-      else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, sm, a.tw, a.lmax);
+      const bool real_ks = a.ks[i].cplx == nullptr;
+      double kn[LN::EPT];  // this input's kernel spectrum, loaded before its transform
+      if (real_ks && valid) {
 #pragma unroll
-      for (int r = 0; r < LN::EPT; ++r)
-        if (valid) y[r] = cadd(y[r], kmul(v[r], a.ks[i], l, LN::out_idx(t, r), LN::M));
+        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[i], l, LN::out_idx(t, r), LN::M);
+      }
+      if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
+      else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+      fft_line<LN, false, HALF>(v, t, sm, twq, L);
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r)
+          y[r] = cadd(y[r], real_ks ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M)
+                                    : kmul(v[r], a.ks[i], l, LN::out_idx(t, r), LN::M));
+      }
     }
-    fft_line<LN, true>(y, t, sm, a.tw, a.lmax);
+    fft_line<LN, true>(y, t, sm, twq, L);
     double2* dst = a.out[0] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
@@ -189,9 +255,9 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   } else {  // OUT_SPECTRUM
 #pragma unroll 1
     for (int i = 0; i < a.n_in; ++i) {
-      if constexpr (IN == IN_SPARSE) load_sparse<LN, LPC, HALF>(v, a, t, l, item, i, valid);
+      if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, sm, a.tw, a.lmax);
+      fft_line<LN, false, HALF>(v, t, sm, twq, L);
       if (!valid) continue;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
@@ -222,7 +288,7 @@ struct LinesArgs {
 
 template <int L, bool INV, bool HALF>
 __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_constant__ LinesArgs a) {
-  using LN = Line<L>;
+  using LN = typename ColCfg<L>::LN;
   constexpr int LPC = ColCfg<L>::LPC;
   extern __shared__ double2 smem[];
   const int line = threadIdx.x % LPC;
@@ -231,6 +297,9 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   const bool valid = l < a.nlines;
   const int c = blockIdx.y;
   double2* sm = smem + line * LN::SMEM;
+  double2* twq = smem + LPC * LN::SMEM;
+  if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
+  __syncthreads();
   const int64_t o = valid ? l / a.inner : 0, q = valid ? l % a.inner : 0;
   const double2* src = a.in[c] + o * a.outer_in + q;
   double2* dst = a.out[c] + o * a.outer_out + q;
@@ -241,7 +310,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
     const int e = INV ? LN::out_idx(t, r) : LN::in_idx(t, r);  // inverse input layout = forward output layout
     v[r] = (valid && e < a.n_valid) ? src[(int64_t)e * a.es_in] : make_double2(0.0, 0.0);
   }
-  fft_line<LN, INV, HALF>(v, t, sm, a.tw, a.lmax);
+  fft_line<LN, INV, HALF>(v, t, sm, twq, L);
   if (!valid) return;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
@@ -364,34 +433,37 @@ template <int LH>
 __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_constant__ GenArgs g, int64_t nrows,
                                                                  double2* out, int64_t out_rs,
                                                                  const double2* tw, int lmax) {
-  using LN = Line<LH>;
+  using LN = typename RowCfg<LH>::LN;
   constexpr int LPC = RowCfg<LH>::LPC;
   constexpr int MH = LN::M;
+  constexpr int LQ = LH + 1;  // quarter table at the resolution of the real row length
   extern __shared__ double2 smem[];
   const int line = threadIdx.x / LN::TPL;
   const int t = threadIdx.x % LN::TPL;
   const int64_t row = (int64_t)blockIdx.x * LPC + line;
   const bool valid = row < nrows;
   double2* sm = smem + line * LN::SMEM;
+  double2* twq = smem + LPC * LN::SMEM;
+  twq_fill(twq, LQ, tw, lmax);
+  __syncthreads();
   double2 v[LN::EPT];
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
     const int m = LN::in_idx(t, r);
     v[r] = valid ? make_double2(gen_value(g, row, 2 * m), gen_value(g, row, 2 * m + 1)) : make_double2(0.0, 0.0);
   }
-  fft_line<LN, false>(v, t, sm, tw, lmax);
+  fft_line<LN, false>(v, t, sm, twq, LQ);
   // natural-order spectrum Z into shared memory, then split into X[k], k in [0, MH]
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) sm[spad(LN::out_idx(t, r))] = v[r];
   __syncthreads();
   if (!valid) return;
-  const int sh = lmax - (LH + 1);
   for (int k = t; k <= MH; k += LN::TPL) {
     const double2 zk = sm[spad(k & (MH - 1))];
     const double2 zc = sm[spad((MH - k) & (MH - 1))];
     const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y - zc.y));   // (Z[k] + conj Z[-k]) / 2
     const double2 d = make_double2(0.5 * (zk.y + zc.y), -0.5 * (zk.x - zc.x));  // (Z[k] - conj Z[-k]) / (2i)
-    const double2 w = __ldg(tw + ((int64_t)k << sh));                          // W_M^k (k = MH -> -1)
+    const double2 w = twq_get(twq, LQ, k);                                     // W_M^k (k = MH -> -1)
     out[row * out_rs + k] = cadd(e, cmul(d, w));
   }
 }
@@ -423,9 +495,9 @@ struct RowArgs {
 
 template <class LN>
 __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* __restrict__ X, int t,
-                                         double2* sm, const double2* __restrict__ tw, int lmax, bool valid) {
+                                         double2* sm, const double2* twq, bool valid) {
   constexpr int MH = LN::M;
-  const int sh = lmax - (LN::L + 1);
+  constexpr int LQ = LN::L + 1;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
     const int k = LN::out_idx(t, r);
@@ -434,18 +506,18 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
       const double2 xb = X[MH - k];  // conj taken below
       const double2 e = make_double2(xa.x + xb.x, xa.y - xb.y);   // X[k] + conj X[MH-k]
       const double2 d = make_double2(xa.x - xb.x, xa.y + xb.y);   // X[k] - conj X[MH-k]
-      const double2 o = cmulc(d, __ldg(tw + ((int64_t)k << sh))); // * W_M^{-k}
+      const double2 o = cmulc(d, twq_get(twq, LQ, k));            // * W_M^{-k}
       z[r] = make_double2(e.x - o.y, e.y + o.x);                  // e + i*o
     } else {
       z[r] = make_double2(0.0, 0.0);
     }
   }
-  fft_line<LN, true>(z, t, sm, tw, lmax);
+  fft_line<LN, true>(z, t, sm, twq, LQ);
 }
 
 template <int LH>
 __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_constant__ RowArgs a) {
-  using LN = Line<LH>;
+  using LN = typename RowCfg<LH>::LN;
   constexpr int LPC = RowCfg<LH>::LPC;
   constexpr int E = LN::EPT;
   extern __shared__ double2 smem[];
@@ -455,6 +527,9 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   const bool valid = row < a.rows;
   const int64_t item = blockIdx.y;
   double2* sm = smem + line * LN::SMEM;
+  double2* twq = smem + LPC * LN::SMEM;
+  twq_fill(twq, LH + 1, a.tw, a.lmax);
+  __syncthreads();
   const int64_t roff = item * a.comp_item + (valid ? (row / a.rows_a) * a.stride_a + (row % a.rows_a) * a.stride_b : 0);
   const int64_t obase = item * a.N + row * a.n_out;
   const bool even = (a.n_out & 1) == 0;
@@ -477,7 +552,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   double2 z[E];
   unsigned cnt = 0;
   if (a.c_phi >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, sm, a.tw, a.lmax, valid);
+    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, sm, twq, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -499,7 +574,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   if (a.c_grad >= 0) {
 #pragma unroll 1
     for (int d = 0; d < a.ngrad; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, sm, a.tw, a.lmax, valid);
+      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, sm, twq, valid);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -512,7 +587,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   if (a.c_hess >= 0) {
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, sm, a.tw, a.lmax, valid);
+      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, sm, twq, valid);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -526,7 +601,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
     }
   }
   if (a.c_sign >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, sm, a.tw, a.lmax, valid);
+    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, sm, twq, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -548,7 +623,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   }
 #pragma unroll 1
   for (int j = 0; j < a.n_raw; ++j) {
-    c2r_line<LN>(z, a.comp[j] + roff, t, sm, a.tw, a.lmax, valid);
+    c2r_line<LN>(z, a.comp[j] + roff, t, sm, twq, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;

@@ -4,11 +4,12 @@ template <int L, int IN, int OUT, bool HALF>
 int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
   using C = ColCfg<L>;
   auto k = col_kernel<L, IN, OUT, HALF>;
-  CK(prep_kernel_attr(k, C::SMEM_BYTES));
+  const size_t smem = C::SMEM_BYTES + (IN == IN_SPARSE ? SPARSE_SMEM : 0);
+  CK(prep_kernel_attr(k, smem));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
   if (tiles <= 0 || items <= 0) return EIK_OK;
   if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
-  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);
+  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, smem, st>>>(a);
   CK(cudaGetLastError());
   return EIK_OK;
 }
