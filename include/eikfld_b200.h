@@ -98,6 +98,10 @@ typedef struct {
  * FftConvolver.__init__/kernel_hat, R/convolution.py:220-251). */
 int eik_plan_create(int dim, const int64_t* counts, double spacing, double tau, uint32_t fields,
                     int device, eik_plan** out);
+/* Same, but the cached kernel spectra cover only the spectral planes
+ * k1 in [k1_begin, k1_begin + k1_count) (3-D slab ranks; k1_count < 0 = all). */
+int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double tau, uint32_t fields,
+                         int device, int64_t k1_begin, int64_t k1_count, eik_plan** out);
 int eik_plan_destroy(eik_plan* plan);
 /* padded[3], spectral lines per item, device bytes held */
 int eik_plan_info(const eik_plan* plan, int64_t* padded, int64_t* lines, int64_t* device_bytes);
@@ -114,6 +118,31 @@ int eik_run(eik_plan* plan, const eik_inputs* in, const eik_outputs* out, uint32
 int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t n_kernels,
                  const int64_t* kshape, const double* field, double* out, uint32_t flags, int device,
                  void* stream);
+
+/* Slab-decomposed 3-D pipeline.  A rank owns the
+ * real-space planes [i0_begin, i0_begin + c0_local) (c0 = G * c0_local) and the
+ * spectral planes k1 in [k1_begin, k1_begin + ks) (M1 = G * ks).  Device
+ * pointers only; complex buffers are interleaved double pairs.  Between the
+ * three passes the caller runs one all-to-all (NCCL) per buffer:
+ *   eik_slab_planes   impulse DFT along axis 2 + FFT along axis 1 of the owned
+ *                     planes (node indices relative to the slab, sorted).  Writes
+ *                     V[i] packed by destination k1-slab: [G][c0_local][ks][H2]
+ *                     (H2 = M2/2+1); group 0: delta_Y (1 buffer), group 1: the
+ *                     three flux components (weights[3 * n_nodes]).
+ *   eik_slab_axis0    after the exchange, V[i] = [c0][ks][H2] for this rank's
+ *                     k1-slab: fused axis-0 FFT, kernel-spectrum multiply and
+ *                     inverse; writes W_j = [c0][ks][H2] per component (group 0:
+ *                     phi + 3 gradient numerators; group 1: the degree sum).
+ *   eik_slab_finish   after the exchange back, W_j = [G][c0_local][ks][H2]:
+ *                     inverse along axis 1, c2r along axis 2 and the epilogue
+ *                     for the owned planes (outputs sized c0_local * c1 * c2).
+ * eik_run on a 3-D plan is exactly these passes with G = 1 and no exchange. */
+int eik_slab_planes(eik_plan* plan, int group, const int64_t* nodes, int64_t n_nodes, const double* weights,
+                    int64_t c0_local, int64_t ks, double* const* v_out, uint32_t flags, void* stream);
+int eik_slab_axis0(eik_plan* plan, int group, double* const* v_in, int64_t k1_begin, int64_t ks,
+                   double* const* w_out, uint32_t flags, void* stream);
+int eik_slab_finish(eik_plan* plan, double* const* w, int64_t c0_local, int64_t ks, const eik_outputs* out,
+                    uint32_t flags, void* stream);
 
 /* Device milliseconds of each pass of the last eik_run issued with
  * EIK_PROFILE (synchronizes on its events); -1 for passes that did not run. */

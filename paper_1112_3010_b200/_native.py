@@ -64,17 +64,27 @@ def lib():
             L.eik_convolve.argtypes = [C.c_int, _i64p, C.c_void_p, C.c_int64, _i64p, C.c_void_p, C.c_void_p,
                                        C.c_uint32, C.c_int, C.c_void_p]
             L.eik_pass_times.argtypes = [C.c_void_p, _f64p, C.c_int]
+            L.eik_plan_create_slab.argtypes = [C.c_int, _i64p, C.c_double, C.c_double, C.c_uint32, C.c_int,
+                                               C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]
+            L.eik_slab_planes.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                          C.c_int64, C.c_void_p, C.c_uint32, C.c_void_p]
+            L.eik_slab_axis0.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                         C.c_uint32, C.c_void_p]
+            L.eik_slab_finish.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs),
+                                          C.c_uint32, C.c_void_p]
             L.eik_last_error.restype = C.c_char_p
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
-                         "eik_version", "eik_pass_times"):
+                         "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
+                         "eik_slab_axis0", "eik_slab_finish"):
                 getattr(L, name).restype = C.c_int
             _lib = L
         return _lib
 
 
 def exported_symbols():
-    return ["eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
-            "eik_pass_times", "eik_last_error", "eik_version"]
+    return ["eik_plan_create", "eik_plan_create_slab", "eik_plan_destroy", "eik_plan_info", "eik_run",
+            "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
+            "eik_last_error", "eik_version"]
 
 
 def check(rc: int):
@@ -99,7 +109,7 @@ def _ptr(a):
 class Plan:
     """Owns one eik_plan: geometry, twiddles and cached kernel spectra on one device."""
 
-    def __init__(self, dim, counts, spacing, tau, fields, device=0):
+    def __init__(self, dim, counts, spacing, tau, fields, device=0, k1_slab=None):
         self.dim = int(dim)
         self.counts = tuple(int(c) for c in counts)
         self.spacing = float(spacing)
@@ -109,7 +119,11 @@ class Plan:
         self.N = int(np.prod(self.counts))
         h = C.c_void_p()
         cnt = (C.c_int64 * 3)(*self.counts, *([1] * (3 - len(self.counts))))
-        check(lib().eik_plan_create(self.dim, cnt, self.spacing, self.tau, self.fields, self.device, C.byref(h)))
+        if k1_slab is None:
+            check(lib().eik_plan_create(self.dim, cnt, self.spacing, self.tau, self.fields, self.device, C.byref(h)))
+        else:
+            check(lib().eik_plan_create_slab(self.dim, cnt, self.spacing, self.tau, self.fields, self.device,
+                                             int(k1_slab[0]), int(k1_slab[1]), C.byref(h)))
         self._h = h
         self._lock = threading.Lock()
 
@@ -119,6 +133,27 @@ class Plan:
         nbytes = C.c_int64()
         check(lib().eik_plan_info(self._h, pad, C.byref(lines), C.byref(nbytes)))
         return {"padded": tuple(pad), "lines": lines.value, "device_bytes": nbytes.value}
+
+    # -- slab-decomposed 3-D passes (device tensors; see include/eikfld_b200.h)
+    def slab_planes(self, group, nodes, weights, c0_local, ks, v_out, stream=None):
+        arr = (C.c_void_p * 3)(*[_ptr(t) for t in v_out], *([None] * (3 - len(v_out))))
+        check(lib().eik_slab_planes(self._h, int(group), _ptr(nodes), int(nodes.shape[0]),
+                                    _ptr(weights), int(c0_local), int(ks), arr, 0, stream))
+
+    def slab_axis0(self, group, v_in, k1_begin, ks, w_out, stream=None):
+        vi = (C.c_void_p * 3)(*[_ptr(t) for t in v_in], *([None] * (3 - len(v_in))))
+        wo = (C.c_void_p * 8)(*[_ptr(t) for t in w_out], *([None] * (8 - len(w_out))))
+        check(lib().eik_slab_axis0(self._h, int(group), vi, int(k1_begin), int(ks), wo, 0, stream))
+
+    def slab_finish(self, w, c0_local, ks, *, S=None, grad=(None, None, None), mu=None, mask=None,
+                    underflow=None, d_count=None, stream=None):
+        wa = (C.c_void_p * 8)(*[_ptr(t) for t in w], *([None] * (8 - len(w))))
+        out = Outputs()
+        out.S, out.mu, out.mask, out.underflow = (_ptr(x) for x in (S, mu, mask, underflow))
+        for d in range(3):
+            out.grad[d] = _ptr(grad[d]) if d < len(grad) else None
+        out.d_underflow_count = _ptr(d_count)
+        check(lib().eik_slab_finish(self._h, wa, int(c0_local), int(ks), C.byref(out), 0, stream))
 
     def pass_times(self):
         """Device ms per pass of the last profiled run ({name: ms}, absent passes omitted)."""

@@ -91,7 +91,9 @@ struct ColArgs {
   // outputs out[j][item*out_item + n*out_es + l]
   double2* out[MAXC];
   int64_t out_es, out_item;
-  // spectrum extraction (OUT_SPECTRUM)
+  // spectrum extraction (OUT_SPECTRUM); SPEC_COMPLEX rows k are split as
+  // (k / out_split) * out_split_stride + (k % out_split) * out_es (slab packing)
+  int64_t out_split, out_split_stride;
   int spec_mode;
   double* spec_re[3];
   int64_t spec_ld;
@@ -263,7 +265,8 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       for (int r = 0; r < LN::EPT; ++r) {
         const int k0 = LN::out_idx(t, r);
         if (a.spec_mode == SPEC_COMPLEX) {
-          a.out[i][item * a.out_item + (int64_t)k0 * a.out_es + l] = v[r];
+          a.out[i][item * a.out_item + (int64_t)(k0 / a.out_split) * a.out_split_stride +
+                   (int64_t)(k0 % a.out_split) * a.out_es + l] = v[r];
         } else if (a.spec_mode == SPEC_COMPLEX_T) {
           a.out[i][(int64_t)k0 * a.spec_ld + l] = v[r];
         } else if (k0 <= (LN::M >> 1)) {
@@ -280,6 +283,7 @@ struct LinesArgs {
   const double2* in[MAXC];
   double2* out[MAXC];
   int64_t nlines, inner, outer_in, outer_out, es_in, es_out;
+  int64_t split, split_stride;  // element e -> (e / split) * split_stride + (e % split) * es
   int n_valid, n_out;
   double scale;
   const double2* tw;
@@ -308,7 +312,8 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   for (int r = 0; r < LN::EPT; ++r) {
     if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
     const int e = INV ? LN::out_idx(t, r) : LN::in_idx(t, r);  // inverse input layout = forward output layout
-    v[r] = (valid && e < a.n_valid) ? src[(int64_t)e * a.es_in] : make_double2(0.0, 0.0);
+    v[r] = (valid && e < a.n_valid) ? src[(e / a.split) * a.split_stride + (e % a.split) * a.es_in]
+                                    : make_double2(0.0, 0.0);
   }
   fft_line<LN, INV, HALF>(v, t, sm, twq, L);
   if (!valid) return;
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
     if (n < a.n_out) {
       double2 x = v[r];
       if (a.scale != 1.0) { x.x *= a.scale; x.y *= a.scale; }
-      dst[(int64_t)n * a.es_out] = x;
+      dst[(n / a.split) * a.split_stride + (n % a.split) * a.es_out] = x;
     }
   }
 }
@@ -474,7 +479,8 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
 struct RowArgs {
   int64_t rows;        // rows per item
   int n_out;           // grid count along the last axis
-  int64_t rows_a, stride_a, stride_b, comp_item;  // row -> (row / rows_a)*stride_a + (row % rows_a)*stride_b
+  int64_t rows_a, stride_a, stride_b, comp_item;  // row -> (row / rows_a)*stride_a + b(row % rows_a)
+  int64_t split, split_stride;                     // b(x) = (x / split)*split_stride + (x % split)*stride_b
   const double2* comp[MAXC];
   int n_comp;
   int c_phi, c_grad, ngrad, c_hess, c_sign, sign_mode, n_raw;  // component slots (-1 absent)
@@ -530,7 +536,9 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   double2* twq = smem + LPC * LN::SMEM;
   twq_fill(twq, LH + 1, a.tw, a.lmax);
   __syncthreads();
-  const int64_t roff = item * a.comp_item + (valid ? (row / a.rows_a) * a.stride_a + (row % a.rows_a) * a.stride_b : 0);
+  const int64_t rb = valid ? row % a.rows_a : 0;
+  const int64_t roff = item * a.comp_item +
+                       (valid ? (row / a.rows_a) * a.stride_a + (rb / a.split) * a.split_stride + (rb % a.split) * a.stride_b : 0);
   const int64_t obase = item * a.N + row * a.n_out;
   const bool even = (a.n_out & 1) == 0;
 

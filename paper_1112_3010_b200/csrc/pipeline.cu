@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -106,6 +107,7 @@ struct eik_plan {
   int dim = 0, D = 0, ref0 = 0;
   int c[3] = {1, 1, 1}, M[3] = {1, 1, 1}, L[3] = {0, 0, 0};
   int64_t N = 0, H = 0, lines = 0;
+  int64_t ks_l0 = 0, ks_lines = 0;  // spectral lines [ks_l0, ks_l0 + ks_lines) whose kernel spectra are stored
   double h = 1.0, tau = 1.0;
   uint32_t fields = 0;
   int device = 0;
@@ -139,6 +141,26 @@ struct eik_plan {
 
 namespace {
 
+constexpr int64_t NOSPLIT = int64_t(1) << 40;
+
+ColArgs col_defaults(const eik_plan* p) {
+  ColArgs a{};
+  a.out_split = NOSPLIT;
+  a.out_split_stride = 0;
+  a.tw = p->tw.as<double2>();
+  a.lmax = p->lmax;
+  return a;
+}
+LinesArgs lines_defaults(const eik_plan* p) {
+  LinesArgs la{};
+  la.split = NOSPLIT;
+  la.split_stride = 0;
+  la.scale = 1.0;
+  la.tw = p->tw.as<double2>();
+  la.lmax = p->lmax;
+  return la;
+}
+
 int setup_geometry(eik_plan* p, int dim, const int64_t* counts, double h) {
   if (dim < 1 || dim > 3) return fail(EIK_EVALIDATION, "dimension must be 1, 2 or 3");
   if (!(h > 0)) return fail(EIK_EVALIDATION, "spacing must be > 0");
@@ -165,6 +187,8 @@ int setup_geometry(eik_plan* p, int dim, const int64_t* counts, double h) {
   const int last = p->D - 1;
   p->H = p->M[last] / 2 + 1;
   p->lines = p->D == 2 ? p->H : (int64_t)p->M[1] * p->H;
+  p->ks_l0 = 0;
+  p->ks_lines = p->lines;
   p->h = h;
   int lm = 2;
   for (int a = 0; a < p->D; ++a) lm = std::max(lm, p->L[a]);
@@ -200,7 +224,7 @@ int spectrum_of(eik_plan* p, const GenArgs& g, int part, double* dst_re, double2
   int rc = launch_r2c(p->L[last] - 1, g, nrows, work, p->H, tw, p->lmax, st);
   if (rc) return rc;
   if (p->D == 3) {
-    LinesArgs la{};
+    LinesArgs la = lines_defaults(p);
     la.in[0] = work;
     la.out[0] = work;
     la.nlines = (int64_t)p->M[0] * p->H;
@@ -214,18 +238,18 @@ int spectrum_of(eik_plan* p, const GenArgs& g, int part, double* dst_re, double2
     rc = launch_lines<false, false>(p->L[1], la, 1, st);
     if (rc) return rc;
   }
-  ColArgs a{};
-  a.nlines = p->lines;
+  ColArgs a = col_defaults(p);
+  a.nlines = p->ks_lines;
   a.n_valid = p->M[0];
   a.n_out = p->M[0];
   a.n_in = 1;
-  a.din[0] = work;
+  a.din[0] = work + p->ks_l0;
   a.din_es = p->lines;
   a.din_item = 0;
   a.spec_mode = part;
   a.spec_re[0] = dst_re;
   a.out[0] = dst_c;
-  a.spec_ld = p->lines;
+  a.spec_ld = p->ks_lines;
   a.tw = tw;
   a.lmax = p->lmax;
   return launch_col<IN_DENSE, OUT_SPECTRUM, false>(p->L[0], a, 1, st);
@@ -238,7 +262,7 @@ int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, in
   k->imag = n_odd_axes % 2;
   k->odd0 = odd0 ? 1 : 0;
   k->sign = sign;
-  const int64_t n = (int64_t)(p->M[0] / 2 + 1) * p->lines;
+  const int64_t n = (int64_t)(p->M[0] / 2 + 1) * p->ks_lines;
   CK(k->buf.ensure(n * sizeof(double)));
   int rc = spectrum_of(p, gen_args(p, ktype, sign), k->imag ? SPEC_IMAG_T : SPEC_REAL_T, k->buf.as<double>(), nullptr,
                        work, st);
@@ -250,17 +274,16 @@ int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, in
 KSpec kspec_of(const eik_plan* p, const KDev& k) {
   KSpec s{};
   s.re = k.buf.as<double>();
-  s.ld = p->lines;
+  s.ld = p->ks_lines;
   s.imag = k.imag;
   s.odd0 = k.odd0;
   return s;
 }
 
-// per-row CSR for a sorted node list (validates order and bounds)
-int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_t K, int64_t items,
-               DevBuf& rowid, DevBuf& cols, DevBuf& rowptr, cudaStream_t st) {
-  const int last = p->D - 1;
-  const int64_t rows_per_item = p->N / p->c[last];
+// per-row CSR for a sorted node list (validates order and bounds): rows of
+// length clast, rows_per_item rows and N_item nodes per item.
+int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_t K, int64_t items, int64_t N_item,
+               int64_t rows_per_item, int64_t clast, DevBuf& rowid, DevBuf& cols, DevBuf& rowptr, cudaStream_t st) {
   const int64_t nrows = rows_per_item * items;
   CK(rowid.ensure(std::max<int64_t>(K, 1) * sizeof(int64_t)));
   CK(cols.ensure(std::max<int64_t>(K, 1) * sizeof(int32_t)));
@@ -270,7 +293,7 @@ int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_
   if (K > 0) {
     const int64_t per = std::max<int64_t>(1, std::min<int64_t>(1024, (K / std::max<int64_t>(items, 1) + 255) / 256));
     prep_nodes_kernel<<<dim3((unsigned)per, (unsigned)items), 256, 0, st>>>(
-        d_nodes, d_off, p->c[last], rows_per_item, p->N, rowid.as<int64_t>(), cols.as<int32_t>(), p->err.as<int>());
+        d_nodes, d_off, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), p->err.as<int>());
     CK(cudaGetLastError());
   }
   rowptr_kernel<<<(unsigned)((nrows + 1 + 255) / 256), 256, 0, st>>>(rowid.as<int64_t>(), K, nrows,
@@ -288,6 +311,11 @@ int eik_version(void) { return 10000; }
 
 int eik_plan_create(int dim, const int64_t* counts, double spacing, double tau, uint32_t fields, int device,
                     eik_plan** out) {
+  return eik_plan_create_slab(dim, counts, spacing, tau, fields, device, 0, -1, out);
+}
+
+int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double tau, uint32_t fields, int device,
+                         int64_t k1_begin, int64_t k1_count, eik_plan** out) {
   if (!out || !counts) return fail(EIK_EVALIDATION, "null argument");
   *out = nullptr;
   if (!(tau > 0)) return fail(EIK_EVALIDATION, "tau must be > 0");
@@ -301,6 +329,13 @@ int eik_plan_create(int dim, const int64_t* counts, double spacing, double tau, 
   p->fields = fields;
   int rc = setup_geometry(p.get(), dim, counts, spacing);
   if (rc) return rc;
+  if (k1_count >= 0) {
+    if (p->D != 3) return fail(EIK_EVALIDATION, "k1 slabs apply to 3-D plans");
+    if (k1_begin < 0 || k1_count < 1 || k1_begin + k1_count > p->M[1])
+      return fail(EIK_EVALIDATION, "k1 slab outside the padded axis");
+    p->ks_l0 = k1_begin * p->H;
+    p->ks_lines = k1_count * p->H;
+  }
   cudaStream_t st = nullptr;
   const bool need_phi = fields & (EIK_FIELD_PHI | EIK_FIELD_S | EIK_FIELD_GRAD | EIK_FIELD_HESS);
   const bool need_sign = fields & (EIK_FIELD_WINDING | EIK_FIELD_DEGREE);
@@ -371,6 +406,192 @@ int eik_plan_info(const eik_plan* p, int64_t* padded, int64_t* lines, int64_t* b
   return EIK_OK;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Pass building blocks shared by eik_run and the slab API.
+
+namespace {
+
+// Which components a run carries, in buffer order [phi, grad..., hess..., sign].
+struct Roles {
+  bool phi = false, hess = false, sign = false;
+  int ngrad = 0;
+  int n_dist() const { return phi ? 1 + ngrad + (hess ? 3 : 0) : 0; }
+  int n_comp() const { return n_dist() + (sign ? 1 : 0); }
+};
+
+int set_components(const eik_plan* p, bool sign_group, const Roles& r, ColArgs& x, double2* const* W,
+                   int64_t k1_offset_lines) {
+  auto ks = [&](const KDev& k) {
+    KSpec s = kspec_of(p, k);
+    s.re += k1_offset_lines - p->ks_l0;  // k1-slab: lines [k1b*H, ...) of the global layout
+    return s;
+  };
+  if (sign_group) {
+    x.n_comp = 1;
+    for (int i = 0; i < x.n_in; ++i) x.ks[i] = ks(*p->ksign[i]);
+    x.out[0] = W[r.n_dist()];
+    return EIK_OK;
+  }
+  int j = 0;
+  x.ks[j] = ks(*p->kdist[p->k_exp]);
+  x.out[j] = W[j];
+  ++j;
+  for (int d = 0; d < r.ngrad; ++d, ++j) { x.ks[j] = ks(*p->kdist[p->k_grad + d]); x.out[j] = W[j]; }
+  if (r.hess)
+    for (int d = 0; d < 3; ++d, ++j) { x.ks[j] = ks(*p->kdist[p->k_hess + d]); x.out[j] = W[j]; }
+  x.n_comp = j;
+  return EIK_OK;
+}
+
+// 2-D: fused column pass of one group straight from the node list.
+int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
+               const Roles& r, double2* const* W, cudaStream_t st) {
+  DevBuf& rid = sg ? p->srowid : p->rowid;
+  DevBuf& cl = sg ? p->scols : p->cols;
+  DevBuf& rp = sg ? p->srowptr : p->rowptr;
+  int rc = prep_nodes(p, nodes, off, K, B, p->N, p->c[0], p->c[1], rid, cl, rp, st);
+  if (rc) return rc;
+  ColArgs a = col_defaults(p);
+  a.rowptr = rp.as<int64_t>();
+  a.cols = cl.as<int32_t>();
+  a.n_in = sg ? p->dim : 1;
+  for (int i = 0; i < 3; ++i) a.w[i] = (sg && i < a.n_in) ? w + (int64_t)i * K : nullptr;
+  a.last_shift = p->lmax - p->L[1];
+  a.last_mask = p->M[1] - 1;
+  a.nlines = p->H;
+  a.n_valid = p->c[0];
+  a.n_out = p->c[0];
+  a.rows_per_item = p->c[0];
+  a.out_es = p->H;
+  a.out_item = p->comp_elems();
+  set_components(p, sg, r, a, W, 0);
+  return sg ? launch_col<IN_SPARSE, OUT_SUM, true>(p->L[0], a, B, st)
+            : launch_col<IN_SPARSE, OUT_COMPS, true>(p->L[0], a, B, st);
+}
+
+// 3-D pass A: impulse DFT along axis 2 + FFT along axis 1 for planes [0, c0loc)
+// of the (slab-relative) node list.  V[i] rows k1 are packed by k1-slab:
+// [k1 / ks][i0][k1 % ks][k2] (ks = M1: plain [i0][k1][k2]).
+int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
+                int64_t c0loc, int64_t ks, double2* const* V, cudaStream_t st) {
+  const int64_t H = p->H, c1 = p->c[1], c2 = p->c[2];
+  DevBuf& rid = sg ? p->srowid : p->rowid;
+  DevBuf& cl = sg ? p->scols : p->cols;
+  DevBuf& rp = sg ? p->srowptr : p->rowptr;
+  int rc = prep_nodes(p, nodes, off, K, B, c0loc * c1 * c2, c0loc * c1, c2, rid, cl, rp, st);
+  if (rc) return rc;
+  ColArgs a = col_defaults(p);
+  a.rowptr = rp.as<int64_t>();
+  a.cols = cl.as<int32_t>();
+  a.n_in = sg ? 3 : 1;
+  for (int i = 0; i < 3; ++i) a.w[i] = (sg && i < a.n_in) ? w + (int64_t)i * K : nullptr;
+  a.last_shift = p->lmax - p->L[2];
+  a.last_mask = p->M[2] - 1;
+  a.nlines = H;
+  a.n_valid = (int)c1;
+  a.rows_per_item = c1;
+  a.spec_mode = SPEC_COMPLEX;
+  a.out_es = H;
+  a.out_item = ks * H;
+  if (ks < p->M[1]) {
+    a.out_split = ks;
+    a.out_split_stride = c0loc * ks * H;
+  }
+  for (int i = 0; i < a.n_in; ++i) a.out[i] = V[i];
+  return launch_col<IN_SPARSE, OUT_SPECTRUM, true>(p->L[1], a, B * c0loc, st);
+}
+
+// 3-D pass B: fused axis-0 pass for k1 in [k1b, k1b + ks) over spectra
+// V[i][i0 < c0][k1'][k2]; writes W_j[n < c0][k1'][k2].
+int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks, int64_t B, const Roles& r,
+               double2* const* W, cudaStream_t st) {
+  const int64_t H = p->H;
+  if (k1b * H < p->ks_l0 || (k1b + ks) * H > p->ks_l0 + p->ks_lines)
+    return fail(EIK_EVALIDATION, "k1 slab not covered by the plan's kernel spectra");
+  ColArgs a = col_defaults(p);
+  a.nlines = ks * H;
+  a.n_valid = p->c[0];
+  a.n_out = p->c[0];
+  a.n_in = sg ? 3 : 1;
+  for (int i = 0; i < a.n_in; ++i) a.din[i] = V[i];
+  a.din_es = ks * H;
+  a.din_item = (int64_t)p->c[0] * ks * H;
+  a.out_es = ks * H;
+  a.out_item = (int64_t)p->c[0] * ks * H;
+  set_components(p, sg, r, a, W, k1b * H);
+  return sg ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st)
+            : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st);
+}
+
+// 3-D pass C (or the 2-D row pass): inverse along axis 1 (3-D only) + c2r along
+// the last axis + epilogue, for planes [0, c0loc).  W_j laid out as
+// [k1 / ks][i0][k1 % ks][k2] (3-D) or [row][k1] (2-D).
+int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, int64_t ks, int64_t B,
+                RowArgs ra, cudaStream_t st, const std::function<int(int, bool)>& mark) {
+  const int64_t H = p->H;
+  const int nc = r.n_comp();
+  int rc;
+  if (p->D == 3) {
+    LinesArgs la = lines_defaults(p);
+    for (int j = 0; j < nc; ++j) { la.in[j] = W[j]; la.out[j] = W[j]; }
+    la.nlines = B * c0loc * H;
+    la.inner = H;
+    la.outer_in = la.outer_out = ks * H;
+    la.es_in = la.es_out = H;
+    if (ks < p->M[1]) {
+      la.split = ks;
+      la.split_stride = c0loc * ks * H;
+    }
+    la.n_valid = p->M[1];
+    la.n_out = p->c[1];
+    if ((rc = mark(EIK_PASS_LINES, false))) return rc;
+    if ((rc = launch_lines<true, false>(p->L[1], la, nc, st))) return rc;
+    if ((rc = mark(EIK_PASS_LINES, true))) return rc;
+    ra.rows = c0loc * p->c[1];
+    ra.rows_a = p->c[1];
+    ra.stride_a = ks * H;
+    ra.stride_b = H;
+    ra.split = ks < p->M[1] ? ks : NOSPLIT;
+    ra.split_stride = ks < p->M[1] ? c0loc * ks * H : 0;
+    ra.comp_item = c0loc * p->M[1] * H;
+    ra.N = c0loc * p->c[1] * p->c[2];
+  } else {
+    ra.rows = p->c[0];
+    ra.rows_a = p->c[0];
+    ra.stride_a = 0;
+    ra.stride_b = H;
+    ra.split = NOSPLIT;
+    ra.split_stride = 0;
+    ra.comp_item = p->comp_elems();
+    ra.N = p->N;
+  }
+  for (int j = 0; j < nc; ++j) ra.comp[j] = W[j];
+  ra.n_comp = nc;
+  ra.n_out = p->c[p->D - 1];
+  ra.c_phi = r.phi ? 0 : -1;
+  ra.c_grad = r.ngrad ? 1 : -1;
+  ra.ngrad = r.ngrad;
+  ra.c_hess = r.hess ? 1 + r.ngrad : -1;
+  ra.c_sign = r.sign ? r.n_dist() : -1;
+  ra.sign_mode = p->dim == 2 ? 1 : 2;
+  double scale = 1.0;
+  for (int a = 0; a < p->D; ++a) scale /= (double)p->M[a];
+  ra.scale = scale;
+  ra.tau = p->tau;
+  ra.inv_tau = 1.0 / p->tau;
+  ra.tw = p->tw.as<double2>();
+  ra.lmax = p->lmax;
+  if ((rc = mark(EIK_PASS_ROW, false))) return rc;
+  if ((rc = launch_row(p->L[p->D - 1] - 1, ra, B, st))) return rc;
+  return mark(EIK_PASS_ROW, true);
+}
+
+}  // namespace
+
+extern "C" {
+
 int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream) {
   if (!p || !in || !out) return fail(EIK_EVALIDATION, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
@@ -393,11 +614,9 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     return fail(EIK_EVALIDATION, "sign field needs weighted nodes");
   if (B > 1 && !in->item_offsets) return fail(EIK_EVALIDATION, "batch > 1 needs item offsets");
 
-  const int D = p->D, last = D - 1;
-  const double2* tw = p->tw.as<double2>();
   const bool prof = flags & EIK_PROFILE;
   for (bool& u : p->ev_used) u = false;
-  auto mark = [&](int pass, bool end) -> int {
+  std::function<int(int, bool)> mark = [&](int pass, bool end) -> int {
     if (!prof) return EIK_OK;
     cudaEvent_t& e = p->ev[2 * pass + (end ? 1 : 0)];
     if (!e) CK(cudaEventCreate(&e));
@@ -410,6 +629,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
   const int64_t* d_off = in->item_offsets;
   const int64_t* d_snodes = in->sign_nodes;
   const double* d_sw = in->sign_weights;
+  const int64_t Ks = in->n_sign_nodes;
   if (want_phi && host_in) {
     CK(p->h_nodes.ensure(in->n_nodes * sizeof(int64_t)));
     CK(cudaMemcpyAsync(p->h_nodes.p, in->nodes, in->n_nodes * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -420,15 +640,12 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
       d_off = p->h_off.as<int64_t>();
     }
   }
-  if (want_phi && B == 1) {
-    if (!d_off || host_in) {
-      const int64_t off[2] = {0, in->n_nodes};
-      CK(cudaMemcpyAsync(p->off1.p, off, sizeof(off), cudaMemcpyHostToDevice, st));
-      d_off = p->off1.as<int64_t>();
-    }
+  if (want_phi && B == 1 && (!d_off || host_in)) {
+    const int64_t off[2] = {0, in->n_nodes};
+    CK(cudaMemcpyAsync(p->off1.p, off, sizeof(off), cudaMemcpyHostToDevice, st));
+    d_off = p->off1.as<int64_t>();
   }
   if (want_sign) {
-    const int64_t Ks = in->n_sign_nodes;
     if (host_in) {
       CK(p->h_snodes.ensure(Ks * sizeof(int64_t)));
       CK(p->h_sw.ensure(Ks * p->dim * sizeof(double)));
@@ -472,170 +689,69 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     o_mu = (double*)fix(o_mu); o_mask = (uint8_t*)fix(o_mask); o_uf = (uint8_t*)fix(o_uf);
   }
   // ---- component buffers
-  const int ngrad = (want_grad || want_hess) ? p->dim : 0;
-  const int n_dist = want_phi ? 1 + ngrad + (want_hess ? 3 : 0) : 0;
-  const int n_comp = n_dist + (want_sign ? 1 : 0);
+  Roles r;
+  r.phi = want_phi;
+  r.ngrad = want_phi && (want_grad || want_hess) ? p->dim : 0;
+  r.hess = want_phi && want_hess;
+  r.sign = want_sign;
+  const int n_comp = r.n_comp();
   const int64_t ce = p->comp_elems();
   CK(p->comp.ensure((size_t)n_comp * B * ce * sizeof(double2)));
-  double2* comp = p->comp.as<double2>();
-  auto compp = [&](int j) { return comp + (int64_t)j * B * ce; };
+  std::vector<double2*> W(n_comp);
+  for (int j = 0; j < n_comp; ++j) W[j] = p->comp.as<double2>() + (int64_t)j * B * ce;
   int rc;
-  const int n_in_sign = p->dim;
-  if (D == 3) CK(p->vin.ensure((size_t)std::max(want_phi ? 1 : 0, want_sign ? n_in_sign : 0) * B * ce * sizeof(double2)));
-  // ---- forward + multiply + first inverse (per group)
-  auto run_group = [&](bool sign_group) -> int {
-    const int64_t K = sign_group ? in->n_sign_nodes : in->n_nodes;
-    DevBuf& rid = sign_group ? p->srowid : p->rowid;
-    DevBuf& cl = sign_group ? p->scols : p->cols;
-    DevBuf& rp = sign_group ? p->srowptr : p->rowptr;
-    const int64_t items = sign_group ? 1 : B;
-    int r = mark(EIK_PASS_PREP, false);
-    if (r) return r;
-    r = prep_nodes(p, sign_group ? d_snodes : d_nodes, sign_group ? p->soff.as<int64_t>() : d_off, K, items, rid, cl,
-                       rp, st);
-    if (r) return r;
-    ColArgs a{};
-    a.rowptr = rp.as<int64_t>();
-    a.cols = cl.as<int32_t>();
-    a.n_in = sign_group ? n_in_sign : 1;
-    for (int i = 0; i < 3; ++i) a.w[i] = (sign_group && i < n_in_sign) ? d_sw + (int64_t)i * K : nullptr;
-    a.last_shift = p->lmax - p->L[last];
-    a.last_mask = p->M[last] - 1;
-    a.tw = tw;
-    a.lmax = p->lmax;
-    if ((r = mark(EIK_PASS_PREP, true))) return r;
-    const int pass = sign_group ? EIK_PASS_COL_SIGN : EIK_PASS_COL;
-    if ((r = mark(pass, false))) return r;
-    const auto& kv = sign_group ? p->ksign : p->kdist;
-    auto set_ks = [&](ColArgs& x) {
-      if (sign_group) {
-        x.n_comp = 1;
-        for (int i = 0; i < n_in_sign; ++i) x.ks[i] = kspec_of(p, *kv[i]);
-        x.out[0] = compp(n_dist);
-      } else {
-        int j = 0;
-        x.ks[j] = kspec_of(p, *kv[p->k_exp]); x.out[j] = compp(j); ++j;
-        for (int d = 0; d < ngrad; ++d, ++j) { x.ks[j] = kspec_of(p, *kv[p->k_grad + d]); x.out[j] = compp(j); }
-        if (want_hess)
-          for (int d = 0; d < 3; ++d, ++j) { x.ks[j] = kspec_of(p, *kv[p->k_hess + d]); x.out[j] = compp(j); }
-        x.n_comp = j;
-      }
-    };
-    if (D == 2) {
-      a.nlines = p->H;
-      a.n_valid = p->c[0];
-      a.n_out = p->c[0];
-      a.rows_per_item = p->c[0];
-      a.out_es = p->H;
-      a.out_item = ce;
-      set_ks(a);
-      r = sign_group ? launch_col<IN_SPARSE, OUT_SUM, true>(p->L[0], a, items, st)
-                     : launch_col<IN_SPARSE, OUT_COMPS, true>(p->L[0], a, items, st);
-      return r ? r : mark(pass, true);
+  if (p->D == 2) {
+    if (want_phi) {
+      if ((rc = mark(EIK_PASS_COL, false))) return rc;
+      if ((rc = pass_col2d(p, false, d_nodes, d_off, in->n_nodes, B, nullptr, r, W.data(), st))) return rc;
+      if ((rc = mark(EIK_PASS_COL, true))) return rc;
     }
-    // 3-D: plane pass (axis 2 impulse DFT + axis 1 FFT) into vin, then axis 0 fused
-    ColArgs pa = a;
-    pa.nlines = p->H;
-    pa.n_valid = p->c[1];
-    pa.rows_per_item = p->c[1];
-    pa.spec_mode = SPEC_COMPLEX;
-    pa.out_es = p->H;
-    pa.out_item = (int64_t)p->M[1] * p->H;
-    double2* V = p->vin.as<double2>();
-    for (int i = 0; i < pa.n_in; ++i) pa.out[i] = V + (int64_t)i * B * ce;
-    r = launch_col<IN_SPARSE, OUT_SPECTRUM, true>(p->L[1], pa, items * p->c[0], st);
-    if (r) return r;
-    ColArgs da{};
-    da.nlines = p->lines;
-    da.n_valid = p->c[0];
-    da.n_out = p->c[0];
-    da.n_in = pa.n_in;
-    for (int i = 0; i < da.n_in; ++i) da.din[i] = V + (int64_t)i * B * ce;
-    da.din_es = p->lines;
-    da.din_item = ce;
-    da.out_es = p->lines;
-    da.out_item = ce;
-    da.tw = tw;
-    da.lmax = p->lmax;
-    set_ks(da);
-    r = sign_group ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], da, items, st)
-                   : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], da, items, st);
-    return r ? r : mark(pass, true);
-  };
-  if (want_phi && (rc = run_group(false))) return rc;
-  if (want_sign && (rc = run_group(true))) return rc;
-  if (D == 3) {  // inverse along axis 1, in place, keep rows [0, c1)
-    LinesArgs la{};
-    for (int j = 0; j < n_comp; ++j) { la.in[j] = compp(j); la.out[j] = compp(j); }
-    la.nlines = B * p->c[0] * p->H;
-    la.inner = p->H;
-    la.outer_in = la.outer_out = (int64_t)p->M[1] * p->H;
-    la.es_in = la.es_out = p->H;
-    la.n_valid = p->M[1];
-    la.n_out = p->c[1];
-    la.scale = 1.0;
-    la.tw = tw;
-    la.lmax = p->lmax;
-    // components of the sign group have batch 1; the comp buffer is laid out per
-    // component with B items, so lines of absent items are simply unused
-    if ((rc = mark(EIK_PASS_LINES, false))) return rc;
-    if ((rc = launch_lines<true, false>(p->L[1], la, n_comp, st))) return rc;
-    if ((rc = mark(EIK_PASS_LINES, true))) return rc;
+    if (want_sign) {
+      if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
+      if ((rc = pass_col2d(p, true, d_snodes, p->soff.as<int64_t>(), Ks, 1, d_sw, r, W.data(), st))) return rc;
+      if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
+    }
+  } else {
+    const int n_in_max = std::max(want_phi ? 1 : 0, want_sign ? 3 : 0);
+    CK(p->vin.ensure((size_t)n_in_max * B * ce * sizeof(double2)));
+    double2* V[3];
+    for (int i = 0; i < 3; ++i) V[i] = p->vin.as<double2>() + (int64_t)i * B * ce;
+    if (want_phi) {
+      if ((rc = mark(EIK_PASS_COL, false))) return rc;
+      if ((rc = pass_planes(p, false, d_nodes, d_off, in->n_nodes, B, nullptr, p->c[0], p->M[1], V, st))) return rc;
+      if ((rc = pass_axis0(p, false, V, 0, p->M[1], B, r, W.data(), st))) return rc;
+      if ((rc = mark(EIK_PASS_COL, true))) return rc;
+    }
+    if (want_sign) {
+      if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
+      if ((rc = pass_planes(p, true, d_snodes, p->soff.as<int64_t>(), Ks, 1, d_sw, p->c[0], p->M[1], V, st)))
+        return rc;
+      if ((rc = pass_axis0(p, true, V, 0, p->M[1], 1, r, W.data(), st))) return rc;
+      if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
+    }
   }
   // ---- last axis c2r + epilogue
   RowArgs ra{};
-  if (D == 2) {
-    ra.rows = p->c[0];
-    ra.rows_a = p->c[0];
-    ra.stride_a = 0;
-    ra.stride_b = p->H;
-  } else {
-    ra.rows = (int64_t)p->c[0] * p->c[1];
-    ra.rows_a = p->c[1];
-    ra.stride_a = (int64_t)p->M[1] * p->H;
-    ra.stride_b = p->H;
-  }
-  ra.comp_item = ce;
-  ra.n_out = p->c[last];
-  for (int j = 0; j < n_comp; ++j) ra.comp[j] = compp(j);
-  ra.n_comp = n_comp;
-  ra.c_phi = want_phi ? 0 : -1;
-  ra.c_grad = ngrad ? 1 : -1;
-  ra.ngrad = ngrad;
-  ra.c_hess = want_hess ? 1 + ngrad : -1;
-  ra.c_sign = want_sign ? n_dist : -1;
-  ra.sign_mode = p->dim == 2 ? 1 : 2;
-  double scale = 1.0;
-  for (int a = 0; a < D; ++a) scale /= (double)p->M[a];
-  ra.scale = scale;
-  ra.tau = p->tau;
-  ra.inv_tau = 1.0 / p->tau;
   ra.S = o_S;
   for (int d = 0; d < 3; ++d) { ra.grad[d] = o_g[d]; ra.hess[d] = o_h[d]; }
   ra.mu = o_mu;
   ra.mask = o_mask;
   ra.uf = o_uf;
   ra.phi_out = o_phi;
-  ra.N = p->N;
   const bool count = want_phi && (out->n_underflow || out->d_underflow_count || (flags & EIK_CHECK_UNDERFLOW));
   unsigned long long* ctr = out->d_underflow_count ? out->d_underflow_count : p->counter.as<unsigned long long>();
   if (count) {
     if (!out->d_underflow_count) CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     ra.uf_count = ctr;
   }
-  ra.tw = tw;
-  ra.lmax = p->lmax;
-  if (want_sign && B > 1) return fail(EIK_EVALIDATION, "sign with batch");
-  if ((rc = mark(EIK_PASS_ROW, false))) return rc;
-  if ((rc = launch_row(p->L[last] - 1, ra, B, st))) return rc;
-  if ((rc = mark(EIK_PASS_ROW, true))) return rc;
+  if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark))) return rc;
   // ---- copy back / sync / checks
   for (auto& s : slots) CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));
   const bool sync = host_out || (flags & (EIK_SYNC | EIK_CHECK_UNDERFLOW)) || out->n_underflow;
   int err_flag = 0;
   unsigned long long nuf = 0;
   if (sync) {
-    if (want_phi || want_sign) CK(cudaMemcpyAsync(&err_flag, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&err_flag, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (count) CK(cudaMemcpyAsync(&nuf, ctr, sizeof(nuf), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (err_flag) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
@@ -644,6 +760,86 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
       return fail(EIK_EUNDERFLOW, "phi has non-positive entries after convolution; increase the precision bits "
                                   "(e.g. --precision big:512) or raise tau");
   }
+  return EIK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Slab-decomposed 3-D pipeline (device pointers only).
+
+static int slab_roles(const eik_plan* p, Roles& r) {
+  if (p->D != 3) return fail(EIK_EVALIDATION, "the slab API is for 3-D grids");
+  r.phi = p->k_exp >= 0;
+  r.ngrad = p->k_grad >= 0 ? 3 : 0;
+  r.hess = false;
+  r.sign = !p->ksign.empty();
+  return EIK_OK;
+}
+
+int eik_slab_planes(eik_plan* p, int group, const int64_t* nodes, int64_t n_nodes, const double* weights,
+                    int64_t c0_local, int64_t ks, double* const* v_out, uint32_t flags, void* stream) {
+  if (!p || !v_out) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  Roles r;
+  int rc = slab_roles(p, r);
+  if (rc) return rc;
+  if (group == 1 && !r.sign) return fail(EIK_EVALIDATION, "plan was built without sign kernels");
+  if (group == 0 && !r.phi) return fail(EIK_EVALIDATION, "plan was built without the distance kernels");
+  if (ks < 1 || p->M[1] % ks || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DevBuf& off = group ? p->soff : p->off1;
+  CK(off.ensure(2 * sizeof(int64_t)));
+  const int64_t o[2] = {0, n_nodes};
+  CK(cudaMemcpyAsync(off.p, o, sizeof(o), cudaMemcpyHostToDevice, st));
+  double2* V[3] = {(double2*)v_out[0], group ? (double2*)v_out[1] : nullptr, group ? (double2*)v_out[2] : nullptr};
+  if ((rc = pass_planes(p, group == 1, nodes, off.as<int64_t>(), n_nodes, 1, weights, c0_local, ks, V, st))) return rc;
+  if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
+  return EIK_OK;
+}
+
+int eik_slab_axis0(eik_plan* p, int group, double* const* v_in, int64_t k1_begin, int64_t ks, double* const* w_out,
+                   uint32_t flags, void* stream) {
+  if (!p || !v_in || !w_out) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  Roles r;
+  int rc = slab_roles(p, r);
+  if (rc) return rc;
+  if (ks < 1 || p->M[1] % ks || k1_begin < 0 || k1_begin + ks > p->M[1]) return fail(EIK_EVALIDATION, "bad slab geometry");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double2* V[3] = {(double2*)v_in[0], group ? (double2*)v_in[1] : nullptr, group ? (double2*)v_in[2] : nullptr};
+  std::vector<double2*> W(r.n_comp(), nullptr);
+  if (group) W[r.n_dist()] = (double2*)w_out[0];
+  else
+    for (int j = 0; j < r.n_dist(); ++j) W[j] = (double2*)w_out[j];
+  if ((rc = pass_axis0(p, group == 1, V, k1_begin, ks, 1, r, W.data(), st))) return rc;
+  if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
+  return EIK_OK;
+}
+
+int eik_slab_finish(eik_plan* p, double* const* w, int64_t c0_local, int64_t ks, const eik_outputs* out,
+                    uint32_t flags, void* stream) {
+  if (!p || !w || !out) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  Roles r;
+  int rc = slab_roles(p, r);
+  if (rc) return rc;
+  if (ks < 1 || p->M[1] % ks || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<double2*> W(r.n_comp());
+  for (int j = 0; j < r.n_comp(); ++j) W[j] = (double2*)w[j];
+  RowArgs ra{};
+  ra.S = out->S;
+  for (int d = 0; d < 3; ++d) ra.grad[d] = out->grad[d];
+  ra.mu = out->mu;
+  ra.mask = out->mask;
+  ra.uf = out->underflow;
+  ra.phi_out = out->phi;
+  if (out->d_underflow_count) ra.uf_count = out->d_underflow_count;
+  std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
+  if ((rc = pass_finish(p, W.data(), r, c0_local, ks, 1, ra, st, nomark))) return rc;
+  if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
   return EIK_OK;
 }
 
@@ -704,7 +900,7 @@ int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t 
   }
   if ((rc = launch_r2c(P.L[last] - 1, gf, trow, Tb.as<double2>(), P.H, tw, P.lmax, st))) return rc;
   if (D == 3) {
-    LinesArgs la{};
+    LinesArgs la = lines_defaults(&P);
     la.in[0] = la.out[0] = Tb.as<double2>();
     la.nlines = (int64_t)P.c[0] * P.H;
     la.inner = P.H;
@@ -721,7 +917,7 @@ int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t 
   for (int a = 0; a < D; ++a) scale /= (double)P.M[a];
   for (int64_t k0 = 0; k0 < n_kernels; k0 += MAXC) {
     const int nk = (int)std::min<int64_t>(MAXC, n_kernels - k0);
-    ColArgs a{};
+    ColArgs a = col_defaults(&P);
     for (int j = 0; j < nk; ++j) {
       GenArgs gk = gen_args(&P, KT_FIELD, 1.0);
       gk.field = d_k + (k0 + j) * kn;
@@ -752,7 +948,7 @@ int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t 
     a.lmax = P.lmax;
     if ((rc = launch_col<IN_DENSE, OUT_COMPS, true>(P.L[0], a, 1, st))) return rc;
     if (D == 3) {
-      LinesArgs la{};
+      LinesArgs la = lines_defaults(&P);
       for (int j = 0; j < nk; ++j) la.in[j] = la.out[j] = a.out[j];
       la.nlines = (int64_t)P.c[0] * P.H;
       la.inner = P.H;
@@ -766,6 +962,7 @@ int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t 
       if ((rc = launch_lines<true, false>(P.L[1], la, nk, st))) return rc;
     }
     RowArgs ra{};
+    ra.split = NOSPLIT;
     if (D == 2) { ra.rows = P.c[0]; ra.rows_a = P.c[0]; ra.stride_b = P.H; }
     else { ra.rows = (int64_t)P.c[0] * P.c[1]; ra.rows_a = P.c[1]; ra.stride_a = (int64_t)P.M[1] * P.H; ra.stride_b = P.H; }
     ra.comp_item = ce;

@@ -1,0 +1,199 @@
+"""Slab-decomposed 3-D distance transform across G ranks (BASELINE config C4).
+
+One process per GPU; torch.distributed (NCCL over NVLink/NVSwitch) moves the
+data.  Rank r owns:
+
+* real-space planes  i0 in [r*c0/G, (r+1)*c0/G)   (c0 divisible by G), and
+* spectral planes    k1 in [r*M1/G, (r+1)*M1/G)   (M1 = padded axis 1).
+
+Per group (distance: delta_Y; sign: the three flux components) the schedule is
+
+  planes  (local)  impulse DFT along axis 2 + FFT along axis 1 of the owned
+                   planes -> V packed by destination k1-slab [G][c0/G][ks][H2]
+  all-to-all       V  -> [c0][ks][H2] on the owner of the k1-slab
+  axis0   (local)  fused axis-0 FFT, kernel-spectrum multiply, inverse per
+                   component -> W_j [c0][ks][H2]
+and then, for all components together,
+  all-to-all       W_j -> [G][c0/G][ks][H2] on the owner of the planes
+  finish  (local)  inverse along axis 1, c2r along axis 2, fused epilogue.
+
+So there is one all-to-all per input and one per component, each moving
+16 * c0 * M1 * H2 bytes over the whole job.  Every pass is
+the same kernel the single-GPU path runs (`eik_run` on a 3-D plan is this
+schedule with G = 1), so a G-rank result is bit-identical to the one-GPU
+result.  Each rank's plan caches only its k1-slab of the kernel spectra.
+
+`run_rank` is written against an executor interface (planes / axis0 /
+finish plus the V/W buffers) and an `exchange(send, recv)` callable, so the
+same orchestration runs with the CUDA executor over NCCL, with several CUDA
+executors emulated in one process (`run_emulated`), and with a numpy
+executor over gloo in the CPU tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ValidationError
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    counts: tuple
+    padded: tuple
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        c0, _, _ = self.counts
+        M1 = self.padded[1]
+        if c0 % self.world or M1 % self.world:
+            raise ValidationError(f"c0={c0} and M1={M1} must be divisible by the {self.world} ranks")
+
+    H = property(lambda self: self.padded[2] // 2 + 1)
+    c0loc = property(lambda self: self.counts[0] // self.world)
+    ks = property(lambda self: self.padded[1] // self.world)
+    i0_begin = property(lambda self: self.rank * self.c0loc)
+    k1_begin = property(lambda self: self.rank * self.ks)
+    block = property(lambda self: self.c0loc * self.ks * self.H)  # complex elements per peer block
+    buf = property(lambda self: self.world * self.block)  # complex elements per V / W buffer
+    plane_nodes = property(lambda self: self.counts[1] * self.counts[2])
+
+    def node_range(self):
+        lo = self.i0_begin * self.plane_nodes
+        return lo, lo + self.c0loc * self.plane_nodes
+
+
+def local_nodes(nodes, layout: SlabLayout, weights=None):
+    """The rank's share of a sorted node list, re-based to its slab; weights (A, K) follow."""
+    nodes = np.asarray(nodes, dtype=np.int64)
+    lo, hi = layout.node_range()
+    a, b = np.searchsorted(nodes, [lo, hi])
+    ln = np.ascontiguousarray(nodes[a:b] - lo)
+    if weights is None:
+        return ln, None
+    return ln, np.ascontiguousarray(np.asarray(weights)[:, a:b])
+
+
+def run_rank(ex, exchange, nodes, sign_nodes=None, sign_weights=None):
+    """One rank of the slab schedule.  `nodes` etc. are this rank's local lists."""
+    ex.planes(0, nodes, None)
+    exchange(ex.V_send[:1], ex.V_recv[:1])
+    ex.axis0(0)
+    if ex.sign and sign_nodes is not None:
+        ex.planes(1, sign_nodes, sign_weights)
+        exchange(ex.V_send[:3], ex.V_recv[:3])
+        ex.axis0(1)
+    exchange(ex.W, ex.W_recv)
+    return ex.finish()
+
+
+def nccl_exchange(dist):
+    """exchange(send, recv) = one all_to_all_single per buffer (equal peer blocks)."""
+
+    def exchange(send, recv):
+        for s, r in zip(send, recv):
+            dist.all_to_all_single(r, s)
+
+    return exchange
+
+
+def run_emulated(executors, node_lists):
+    """All ranks in one process: phase by phase, exchanges as block copies.
+
+    node_lists[r] = (nodes, sign_nodes, sign_weights) local to rank r.  Only
+    for testing the decomposition on one device (no rank ever waits on another).
+    """
+    G = len(executors)
+
+    def swap(get_send, get_recv, n):
+        for i in range(n):
+            for r in range(G):
+                recv = get_recv(executors[r])[i].view(G, -1)
+                for g in range(G):
+                    recv[g].copy_(get_send(executors[g])[i].view(G, -1)[r])
+
+    for r, ex in enumerate(executors):
+        ex.planes(0, node_lists[r][0], None)
+    swap(lambda e: e.V_send, lambda e: e.V_recv, 1)
+    for ex in executors:
+        ex.axis0(0)
+    if executors[0].sign and node_lists[0][1] is not None:
+        for r, ex in enumerate(executors):
+            ex.planes(1, node_lists[r][1], node_lists[r][2])
+        swap(lambda e: e.V_send, lambda e: e.V_recv, 3)
+        for ex in executors:
+            ex.axis0(1)
+    swap(lambda e: e.W, lambda e: e.W_recv, len(executors[0].W))
+    return [ex.finish() for ex in executors]
+
+
+class CudaSlabExecutor:
+    """CUDA passes of one rank (libeikfld_b200 slab API) with torch device buffers."""
+
+    def __init__(self, grid, tau, world, rank, *, grad=True, sign=True, device=0):
+        import torch
+
+        from . import _native
+        from .engine import field_bits
+
+        if len(grid.counts) != 3:
+            raise ValidationError("the slab decomposition is for 3-D grids")
+        probe = _native.Plan(3, grid.counts, grid.spacing, tau, 0, device)
+        padded = probe.info()["padded"]
+        probe.close()
+        self.layout = SlabLayout(tuple(grid.counts), tuple(padded), world, rank)
+        L = self.layout
+        self.sign = sign
+        self.grad = grad
+        self.dev = torch.device("cuda", device)
+        self.plan = _native.Plan(3, grid.counts, grid.spacing, tau, field_bits(3, grad, False, sign), device,
+                                 k1_slab=(L.k1_begin, L.ks))
+        n = 2 * L.buf  # doubles per complex buffer
+        mk = lambda: torch.empty((L.world, n // L.world), dtype=torch.float64, device=self.dev)  # noqa: E731
+        n_in = 3 if sign else 1
+        self.n_dist = 1 + (3 if grad else 0)
+        n_comp = self.n_dist + (1 if sign else 0)
+        self.V_send = [mk() for _ in range(n_in)]
+        self.V_recv = [mk() for _ in range(n_in)]
+        self.W = [mk() for _ in range(n_comp)]
+        self.W_recv = [mk() for _ in range(n_comp)]
+        self.N_local = L.c0loc * L.plane_nodes
+
+    def _stream(self):
+        import torch
+
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def planes(self, group, nodes, weights):
+        import torch
+
+        L = self.layout
+        nd = torch.as_tensor(np.ascontiguousarray(nodes, dtype=np.int64), device=self.dev)
+        wt = None if weights is None else torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float64),
+                                                          device=self.dev)
+        self._keep = (nd, wt)
+        self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, self.V_send[:3 if group else 1], self._stream())
+
+    def axis0(self, group):
+        L = self.layout
+        out = [self.W[self.n_dist]] if group else self.W[: self.n_dist]
+        self.plan.slab_axis0(group, self.V_recv[:3 if group else 1], L.k1_begin, L.ks, out, self._stream())
+
+    def finish(self):
+        import torch
+
+        L = self.layout
+        f = lambda: torch.empty(self.N_local, dtype=torch.float64, device=self.dev)  # noqa: E731
+        out = {"S": f(), "underflow": torch.empty(self.N_local, dtype=torch.uint8, device=self.dev)}
+        if self.grad:
+            out["grad"] = [f() for _ in range(3)]
+        if self.sign:
+            out["mu"] = f()
+            out["mask"] = torch.empty(self.N_local, dtype=torch.uint8, device=self.dev)
+        self.plan.slab_finish(self.W_recv, L.c0loc, L.ks, S=out["S"], grad=out.get("grad", (None,) * 3),
+                              mu=out.get("mu"), mask=out.get("mask"), underflow=out["underflow"],
+                              stream=self._stream())
+        return out

@@ -1,0 +1,91 @@
+"""Numpy executor of the slab schedule (TEST INFRASTRUCTURE).
+
+Implements the three slab passes of paper_1112_3010_b200.slab with numpy FFTs
+on exactly the buffer layouts the CUDA passes use, so the orchestration
+(node partitioning, packing, all-to-all exchanges, reassembly) can be tested
+on CPU ranks over gloo.  Kernel samples come from the oracle.
+"""
+
+import math
+
+import numpy as np
+
+import eikfld_oracle as orc
+from paper_1112_3010_b200.slab import SlabLayout
+
+
+def _nextpow2(n):
+    return 1 << max(1, int(n - 1).bit_length())
+
+
+def _wrap(centred, counts, padded):
+    out = np.zeros(padded)
+    idx = [np.r_[0:c, M - (c - 1):M] for c, M in zip(counts, padded)]
+    src = [np.r_[c - 1:2 * c - 1, 0:c - 1] for c in counts]
+    out[np.ix_(*idx)] = centred[np.ix_(*src)]
+    return out
+
+
+class NumpySlabExecutor:
+    def __init__(self, counts, spacing, tau, world, rank, grad=True, sign=True):
+        padded = tuple(_nextpow2(2 * c - 1) for c in counts)
+        self.layout = L = SlabLayout(tuple(counts), padded, world, rank)
+        self.tau, self.grad, self.sign = tau, grad, sign
+        base = orc.kernel_exp(counts, spacing, tau)
+        fa, _ = orc.directional_kernels(counts, spacing)
+        kern = [base] + ([f * base for f in fa] if grad else [])
+        sl = slice(L.k1_begin, L.k1_begin + L.ks)
+        self.kd = [np.fft.rfftn(_wrap(k, counts, padded))[:, sl, :] for k in kern]
+        self.ksg = [np.fft.rfftn(_wrap(orc.ratio_kernel(counts, spacing, a, 3), counts, padded))[:, sl, :]
+                    for a in range(3)] if sign else []
+        mk = lambda: np.zeros((L.world, L.block), dtype=np.complex128)  # noqa: E731
+        n_in = 3 if sign else 1
+        self.n_dist = len(kern)
+        self.V_send = [mk() for _ in range(n_in)]
+        self.V_recv = [mk() for _ in range(n_in)]
+        self.W = [mk() for _ in range(self.n_dist + (1 if sign else 0))]
+        self.W_recv = [mk() for _ in range(len(self.W))]
+
+    def planes(self, group, nodes, weights):
+        L = self.layout
+        c0, c1, c2 = L.counts
+        M0, M1, M2 = L.padded
+        n_in = 3 if group else 1
+        for i in range(n_in):
+            g = np.zeros(L.c0loc * c1 * c2)
+            np.add.at(g, nodes, 1.0 if weights is None else weights[i])
+            t = np.fft.fft(np.fft.rfft(g.reshape(L.c0loc, c1, c2), n=M2, axis=2), n=M1, axis=1)
+            for dest in range(L.world):
+                self.V_send[i][dest] = t[:, dest * L.ks:(dest + 1) * L.ks, :].reshape(-1)
+
+    def axis0(self, group):
+        L = self.layout
+        c0 = L.counts[0]
+        M0 = L.padded[0]
+        n_in = 3 if group else 1
+        X = [np.fft.fft(self.V_recv[i].reshape(c0, L.ks, L.H), n=M0, axis=0) for i in range(n_in)]
+        if group:
+            Y = [sum(k * x for k, x in zip(self.ksg, X))]
+            dst = [self.W[self.n_dist]]
+        else:
+            Y = [k * X[0] for k in self.kd]
+            dst = self.W[: self.n_dist]
+        for y, d in zip(Y, dst):
+            d[:] = np.fft.ifft(y, axis=0)[:c0].reshape(L.world, L.block)
+
+    def finish(self):
+        L = self.layout
+        c0, c1, c2 = L.counts
+        M0, M1, M2 = L.padded
+        comps = []
+        for w in self.W_recv:
+            a = w.reshape(L.world, L.c0loc, L.ks, L.H).transpose(1, 0, 2, 3).reshape(L.c0loc, M1, L.H)
+            a = np.fft.ifft(a, axis=1)[:, :c1, :]
+            comps.append(np.fft.irfft(a, n=M2, axis=2)[:, :, :c2].reshape(-1))
+        phi = comps[0]
+        out = {"phi": phi, "S": -self.tau * np.log(np.where(phi > 0, phi, np.nan))}
+        if self.grad:
+            out["grad"] = [c / phi for c in comps[1:4]]
+        if self.sign:
+            out["mu"] = -comps[-1] / (4.0 * math.pi)
+        return out
