@@ -159,7 +159,11 @@ class CudaSlabExecutor:
         self.V_send = [mk() for _ in range(n_in)]
         self.V_recv = [mk() for _ in range(n_in)]
         self.W = [mk() for _ in range(n_comp)]
-        self.W_recv = [mk() for _ in range(n_comp)]
+        # the spectra V are dead once both axis-0 passes ran: the returned
+        # components reuse them (5 + 6 buffers of c0/G * M1 * H2 complex per rank
+        # instead of 5 + 5 + 6 -> C4 1024^3 fits 4 or more B200s)
+        spare = self.V_send + self.V_recv
+        self.W_recv = [spare[j] if j < len(spare) else mk() for j in range(n_comp)]
         self.N_local = L.c0loc * L.plane_nodes
 
     def _stream(self):
@@ -171,9 +175,14 @@ class CudaSlabExecutor:
         import torch
 
         L = self.layout
-        nd = torch.as_tensor(np.ascontiguousarray(nodes, dtype=np.int64), device=self.dev)
-        wt = None if weights is None else torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float64),
-                                                          device=self.dev)
+
+        def dev(x, dt):
+            if x is None or isinstance(x, torch.Tensor):
+                return x
+            return torch.as_tensor(np.ascontiguousarray(x, dtype=dt), device=self.dev)
+
+        nd = dev(nodes, np.int64)
+        wt = dev(weights, np.float64)
         self._keep = (nd, wt)
         self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, self.V_send[:3 if group else 1], self._stream())
 

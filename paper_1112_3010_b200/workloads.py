@@ -157,11 +157,21 @@ def vertex_area_normals(verts, faces):
     return out
 
 
-def c4(seed: int = 0, n: int = 1024, freq: int = 224, radius: float = 350.0):
+def c4(seed: int = 0, n: int = 1024, freq: int | None = None, radius: float | None = None):
+    """Perturbed icosphere in an origin-centred n^3 grid; at n = 1024: radius 350,
+    frequency 224 (501,762 vertices).  Smaller n scales radius and frequency."""
+    freq = freq if freq is not None else max(4, round(224 * n / 1024))
+    radius = radius if radius is not None else 350.0 * n / 1024
     grid = GridSpec((-(n - 1) / 2.0,) * 3, 1.0, (n, n, n))
     v, f = perturbed_sphere(seed, freq, radius)
     w = vertex_area_normals(v, f)
-    return {"grid": grid, "tau": 0.75, "vertices": v, "faces": f, "weights": w}
+    idx = snap_points(v, grid).snapped_indices
+    nodes, inv = np.unique(idx, return_inverse=True)
+    acc = np.zeros((3, nodes.size))
+    for a in range(3):
+        np.add.at(acc[a], inv, w[:, a])
+    return {"grid": grid, "tau": 0.75, "vertices": v, "faces": f, "weights": w,
+            "nodes": nodes, "sign_nodes": nodes, "sign_weights": acc}
 
 
 def surface_from_mesh(v, f) -> Surface3D:
