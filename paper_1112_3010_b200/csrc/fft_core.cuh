@@ -181,11 +181,27 @@ struct Line {
   __device__ static __forceinline__ constexpr bool upper_in(int i) { return (i % R0) >= (R0 / 2); }
 };
 
+// Exchange buffers of one line.  With NBUF = 2 consecutive exchanges alternate
+// between two buffers, so a stage needs one __syncthreads (between its writes
+// and its reads) instead of two: writes of exchange k+2 cannot overtake reads
+// of exchange k because every thread passed the barrier of exchange k+1.
+template <int NBUF>
+struct XBuf {
+  double2* b0;
+  double2* b1;
+  int ph;
+  __device__ __forceinline__ double2* cur() const { return (NBUF == 2 && ph) ? b1 : b0; }
+  __device__ __forceinline__ void done() {
+    if constexpr (NBUF == 2) ph ^= 1;
+    else __syncthreads();
+  }
+};
+
 // One Stockham stage S of direction INV, followed (if not last) by the
 // shared-memory exchange into the next stage's register layout.
 // twq: shared quarter table at resolution 2^lq (lq >= L).
-template <class LN, bool INV, int S, bool HALF_IN>
-__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm, const double2* twq, int lq) {
+template <class LN, bool INV, int S, bool HALF_IN, class XB>
+__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, const double2* twq, int lq) {
   constexpr int R = LN::rad(INV, S);
   constexpr int NS = LN::ns(INV, S);
   constexpr int G = LN::EPT / R;
@@ -204,6 +220,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm,
     dft<R, INV, HALF_IN && S == 0>(&v[g * R]);
   }
   if constexpr (S + 1 < LN::NST) {
+    double2* sm = xb.cur();
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int b = t + g * LN::TPL;
@@ -220,24 +237,24 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, double2* sm,
 #pragma unroll
       for (int r = 0; r < R2; ++r) v[g * R2 + r] = sm[spad(b + r * (LN::M / R2))];
     }
-    __syncthreads();
+    xb.done();
   }
 }
 
-template <class LN, bool INV, int S, bool HALF_IN>
-__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, double2* sm, const double2* twq, int lq) {
+template <class LN, bool INV, int S, bool HALF_IN, class XB>
+__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, XB& xb, const double2* twq, int lq) {
   if constexpr (S < LN::NST) {
-    stage<LN, INV, S, HALF_IN>(v, t, sm, twq, lq);
-    stages_from<LN, INV, S + 1, HALF_IN>(v, t, sm, twq, lq);
+    stage<LN, INV, S, HALF_IN>(v, t, xb, twq, lq);
+    stages_from<LN, INV, S + 1, HALF_IN>(v, t, xb, twq, lq);
   }
 }
 
 // Full transform of the line held in v (layouts documented above).
 // HALF_IN (forward only): input elements >= M/2 are zero and their registers are not read.
-template <class LN, bool INV, bool HALF_IN = false>
-__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, double2* sm, const double2* twq, int lq) {
+template <class LN, bool INV, bool HALF_IN = false, class XB>
+__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const double2* twq, int lq) {
   static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
-  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, sm, twq, lq);
+  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, twq, lq);
 }
 
 }  // namespace eik

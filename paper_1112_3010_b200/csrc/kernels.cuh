@@ -46,7 +46,11 @@ struct ColCfg {
   using LN = Line<L, col_e(L)>;
   static constexpr int NT = (col_threads(L) > LN::TPL) ? col_threads(L) : LN::TPL;
   static constexpr int LPC = NT / LN::TPL;
-  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ) * sizeof(double2);
+  // ping-pong exchange buffers (one barrier per exchange instead of two) where
+  // they were measured to pay off without costing occupancy (C5-sized lines)
+  static constexpr int NBUF = ((L == 10 || L == 11) && (2 * LPC * LN::SMEM + LN::TWQ) * 16 <= 200 * 1024) ? 2 : 1;
+  using XB = XBuf<NBUF>;
+  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + LN::TWQ) * sizeof(double2);
 };
 // Row kernels (c2r / r2c along the contiguous last axis): complex lines of
 // length 2^LH = M_last/2, quarter table at the resolution of M_last.
@@ -57,7 +61,9 @@ struct RowCfg {
   static constexpr int NT = (LN::TPL >= 128) ? LN::TPL : 128;
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
-  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + TWQ) * sizeof(double2);
+  static constexpr int NBUF = (LH <= 10 && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
+  using XB = XBuf<NBUF>;
+  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ) * sizeof(double2);
 };
 
 // Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
@@ -92,8 +98,10 @@ struct ColArgs {
   double2* out[MAXC];
   int64_t out_es, out_item;
   // spectrum extraction (OUT_SPECTRUM); SPEC_COMPLEX rows k are split as
-  // (k / out_split) * out_split_stride + (k % out_split) * out_es (slab packing)
-  int64_t out_split, out_split_stride;
+  // (k >> out_split_shift) * out_split_stride + (k & (2^shift - 1)) * out_es
+  // (slab packing; shift 30 = no split)
+  int out_split_shift;
+  int64_t out_split_stride;
   int spec_mode;
   double* spec_re[3];
   int64_t spec_ld;
@@ -185,8 +193,9 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   const int64_t l = (int64_t)blockIdx.x * LPC + line;
   const bool valid = l < a.nlines;
   const int64_t item = blockIdx.y;
-  double2* sm = smem + line * LN::SMEM;
-  double2* twq = smem + LPC * LN::SMEM;
+  using CC = ColCfg<L>;
+  typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
+  double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   __syncthreads();
 
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   if constexpr (OUT == OUT_COMPS) {
     if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
     else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
-    fft_line<LN, false, HALF>(v, t, sm, twq, L);
+    fft_line<LN, false, HALF>(v, t, xb, twq, L);
     const bool real_ks = a.ks[0].cplx == nullptr;
     double kn[LN::EPT];  // next component's kernel spectrum, prefetched
     if (real_ks && valid) {
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kmul(v[r], a.ks[j], l, LN::out_idx(t, r), LN::M) : v[r];
       }
-      fft_line<LN, true>(y, t, sm, twq, L);
+      fft_line<LN, true>(y, t, xb, twq, L);
       double2* dst = a.out[j] + item * a.out_item + l;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, sm, twq, L);
+      fft_line<LN, false, HALF>(v, t, xb, twq, L);
       if (valid) {
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r)
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
                                     : kmul(v[r], a.ks[i], l, LN::out_idx(t, r), LN::M));
       }
     }
-    fft_line<LN, true>(y, t, sm, twq, L);
+    fft_line<LN, true>(y, t, xb, twq, L);
     double2* dst = a.out[0] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
@@ -259,14 +268,14 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     for (int i = 0; i < a.n_in; ++i) {
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, sm, twq, L);
+      fft_line<LN, false, HALF>(v, t, xb, twq, L);
       if (!valid) continue;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
         const int k0 = LN::out_idx(t, r);
         if (a.spec_mode == SPEC_COMPLEX) {
-          a.out[i][item * a.out_item + (int64_t)(k0 / a.out_split) * a.out_split_stride +
-                   (int64_t)(k0 % a.out_split) * a.out_es + l] = v[r];
+          a.out[i][item * a.out_item + (int64_t)(k0 >> a.out_split_shift) * a.out_split_stride +
+                   (int64_t)(k0 & ((1 << a.out_split_shift) - 1)) * a.out_es + l] = v[r];
         } else if (a.spec_mode == SPEC_COMPLEX_T) {
           a.out[i][(int64_t)k0 * a.spec_ld + l] = v[r];
         } else if (k0 <= (LN::M >> 1)) {
@@ -283,7 +292,8 @@ struct LinesArgs {
   const double2* in[MAXC];
   double2* out[MAXC];
   int64_t nlines, inner, outer_in, outer_out, es_in, es_out;
-  int64_t split, split_stride;  // element e -> (e / split) * split_stride + (e % split) * es
+  int split_shift;              // element e -> (e >> shift) * split_stride + (e & (2^shift - 1)) * es
+  int64_t split_stride;
   int n_valid, n_out;
   double scale;
   const double2* tw;
@@ -300,8 +310,9 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   const int64_t l = (int64_t)blockIdx.x * LPC + line;
   const bool valid = l < a.nlines;
   const int c = blockIdx.y;
-  double2* sm = smem + line * LN::SMEM;
-  double2* twq = smem + LPC * LN::SMEM;
+  using CC = ColCfg<L>;
+  typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
+  double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   __syncthreads();
   const int64_t o = valid ? l / a.inner : 0, q = valid ? l % a.inner : 0;
@@ -312,10 +323,11 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   for (int r = 0; r < LN::EPT; ++r) {
     if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
     const int e = INV ? LN::out_idx(t, r) : LN::in_idx(t, r);  // inverse input layout = forward output layout
-    v[r] = (valid && e < a.n_valid) ? src[(e / a.split) * a.split_stride + (e % a.split) * a.es_in]
-                                    : make_double2(0.0, 0.0);
+    v[r] = (valid && e < a.n_valid)
+               ? src[(int64_t)(e >> a.split_shift) * a.split_stride + (int64_t)(e & ((1 << a.split_shift) - 1)) * a.es_in]
+               : make_double2(0.0, 0.0);
   }
-  fft_line<LN, INV, HALF>(v, t, sm, twq, L);
+  fft_line<LN, INV, HALF>(v, t, xb, twq, L);
   if (!valid) return;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
     if (n < a.n_out) {
       double2 x = v[r];
       if (a.scale != 1.0) { x.x *= a.scale; x.y *= a.scale; }
-      dst[(n / a.split) * a.split_stride + (n % a.split) * a.es_out] = x;
+      dst[(int64_t)(n >> a.split_shift) * a.split_stride + (int64_t)(n & ((1 << a.split_shift) - 1)) * a.es_out] = x;
     }
   }
 }
@@ -447,8 +459,9 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
   const int t = threadIdx.x % LN::TPL;
   const int64_t row = (int64_t)blockIdx.x * LPC + line;
   const bool valid = row < nrows;
-  double2* sm = smem + line * LN::SMEM;
-  double2* twq = smem + LPC * LN::SMEM;
+  using RC = RowCfg<LH>;
+  typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
+  double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
   twq_fill(twq, LQ, tw, lmax);
   __syncthreads();
   double2 v[LN::EPT];
@@ -457,8 +470,10 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
     const int m = LN::in_idx(t, r);
     v[r] = valid ? make_double2(gen_value(g, row, 2 * m), gen_value(g, row, 2 * m + 1)) : make_double2(0.0, 0.0);
   }
-  fft_line<LN, false>(v, t, sm, twq, LQ);
-  // natural-order spectrum Z into shared memory, then split into X[k], k in [0, MH]
+  fft_line<LN, false>(v, t, xb, twq, LQ);
+  // natural-order spectrum Z into shared memory (the buffer the last exchange
+  // did not use), then split into X[k], k in [0, MH]
+  double2* sm = xb.cur();
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) sm[spad(LN::out_idx(t, r))] = v[r];
   __syncthreads();
@@ -480,7 +495,8 @@ struct RowArgs {
   int64_t rows;        // rows per item
   int n_out;           // grid count along the last axis
   int64_t rows_a, stride_a, stride_b, comp_item;  // row -> (row / rows_a)*stride_a + b(row % rows_a)
-  int64_t split, split_stride;                     // b(x) = (x / split)*split_stride + (x % split)*stride_b
+  int split_shift;                                 // b(x) = (x >> shift)*split_stride + (x & (2^shift-1))*stride_b
+  int64_t split_stride;
   const double2* comp[MAXC];
   int n_comp;
   int c_phi, c_grad, ngrad, c_hess, c_sign, sign_mode, n_raw;  // component slots (-1 absent)
@@ -499,9 +515,9 @@ struct RowArgs {
   int lmax;
 };
 
-template <class LN>
+template <class LN, class XB>
 __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* __restrict__ X, int t,
-                                         double2* sm, const double2* twq, bool valid) {
+                                         XB& xb, const double2* twq, bool valid) {
   constexpr int MH = LN::M;
   constexpr int LQ = LN::L + 1;
 #pragma unroll
@@ -518,7 +534,7 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
       z[r] = make_double2(0.0, 0.0);
     }
   }
-  fft_line<LN, true>(z, t, sm, twq, LQ);
+  fft_line<LN, true>(z, t, xb, twq, LQ);
 }
 
 template <int LH>
@@ -532,13 +548,16 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   const int64_t row = (int64_t)blockIdx.x * LPC + line;
   const bool valid = row < a.rows;
   const int64_t item = blockIdx.y;
-  double2* sm = smem + line * LN::SMEM;
-  double2* twq = smem + LPC * LN::SMEM;
+  using RC = RowCfg<LH>;
+  typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
+  double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
   twq_fill(twq, LH + 1, a.tw, a.lmax);
   __syncthreads();
   const int64_t rb = valid ? row % a.rows_a : 0;
   const int64_t roff = item * a.comp_item +
-                       (valid ? (row / a.rows_a) * a.stride_a + (rb / a.split) * a.split_stride + (rb % a.split) * a.stride_b : 0);
+                       (valid ? (row / a.rows_a) * a.stride_a + (rb >> a.split_shift) * a.split_stride +
+                                    (rb & ((int64_t(1) << a.split_shift) - 1)) * a.stride_b
+                              : 0);
   const int64_t obase = item * a.N + row * a.n_out;
   const bool even = (a.n_out & 1) == 0;
 
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   double2 z[E];
   unsigned cnt = 0;
   if (a.c_phi >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, sm, twq, valid);
+    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, xb, twq, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -582,7 +601,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   if (a.c_grad >= 0) {
 #pragma unroll 1
     for (int d = 0; d < a.ngrad; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, sm, twq, valid);
+      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, xb, twq, valid);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -595,7 +614,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   if (a.c_hess >= 0) {
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, sm, twq, valid);
+      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, xb, twq, valid);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -609,7 +628,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
     }
   }
   if (a.c_sign >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, sm, twq, valid);
+    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, xb, twq, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -631,7 +650,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_consta
   }
 #pragma unroll 1
   for (int j = 0; j < a.n_raw; ++j) {
-    c2r_line<LN>(z, a.comp[j] + roff, t, sm, twq, valid);
+    c2r_line<LN>(z, a.comp[j] + roff, t, xb, twq, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;

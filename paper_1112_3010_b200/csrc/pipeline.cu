@@ -141,11 +141,11 @@ struct eik_plan {
 
 namespace {
 
-constexpr int64_t NOSPLIT = int64_t(1) << 40;
+constexpr int NOSPLIT = 30;  // split shift meaning "no split"
 
 ColArgs col_defaults(const eik_plan* p) {
   ColArgs a{};
-  a.out_split = NOSPLIT;
+  a.out_split_shift = NOSPLIT;
   a.out_split_stride = 0;
   a.tw = p->tw.as<double2>();
   a.lmax = p->lmax;
@@ -153,7 +153,7 @@ ColArgs col_defaults(const eik_plan* p) {
 }
 LinesArgs lines_defaults(const eik_plan* p) {
   LinesArgs la{};
-  la.split = NOSPLIT;
+  la.split_shift = NOSPLIT;
   la.split_stride = 0;
   la.scale = 1.0;
   la.tw = p->tw.as<double2>();
@@ -496,7 +496,7 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
   a.out_es = H;
   a.out_item = ks * H;
   if (ks < p->M[1]) {
-    a.out_split = ks;
+    a.out_split_shift = ilog2_exact(ks);
     a.out_split_stride = c0loc * ks * H;
   }
   for (int i = 0; i < a.n_in; ++i) a.out[i] = V[i];
@@ -541,7 +541,7 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
     la.outer_in = la.outer_out = ks * H;
     la.es_in = la.es_out = H;
     if (ks < p->M[1]) {
-      la.split = ks;
+      la.split_shift = ilog2_exact(ks);
       la.split_stride = c0loc * ks * H;
     }
     la.n_valid = p->M[1];
@@ -553,7 +553,7 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
     ra.rows_a = p->c[1];
     ra.stride_a = ks * H;
     ra.stride_b = H;
-    ra.split = ks < p->M[1] ? ks : NOSPLIT;
+    ra.split_shift = ks < p->M[1] ? ilog2_exact(ks) : NOSPLIT;
     ra.split_stride = ks < p->M[1] ? c0loc * ks * H : 0;
     ra.comp_item = c0loc * p->M[1] * H;
     ra.N = c0loc * p->c[1] * p->c[2];
@@ -562,7 +562,7 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
     ra.rows_a = p->c[0];
     ra.stride_a = 0;
     ra.stride_b = H;
-    ra.split = NOSPLIT;
+    ra.split_shift = NOSPLIT;
     ra.split_stride = 0;
     ra.comp_item = p->comp_elems();
     ra.N = p->N;
@@ -785,7 +785,7 @@ int eik_slab_planes(eik_plan* p, int group, const int64_t* nodes, int64_t n_node
   if (rc) return rc;
   if (group == 1 && !r.sign) return fail(EIK_EVALIDATION, "plan was built without sign kernels");
   if (group == 0 && !r.phi) return fail(EIK_EVALIDATION, "plan was built without the distance kernels");
-  if (ks < 1 || p->M[1] % ks || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
+  if (ks < 1 || p->M[1] % ks || (ks & (ks - 1)) || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   DevBuf& off = group ? p->soff : p->off1;
   CK(off.ensure(2 * sizeof(int64_t)));
@@ -962,7 +962,7 @@ int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t 
       if ((rc = launch_lines<true, false>(P.L[1], la, nk, st))) return rc;
     }
     RowArgs ra{};
-    ra.split = NOSPLIT;
+    ra.split_shift = NOSPLIT;
     if (D == 2) { ra.rows = P.c[0]; ra.rows_a = P.c[0]; ra.stride_b = P.H; }
     else { ra.rows = (int64_t)P.c[0] * P.c[1]; ra.rows_a = P.c[1]; ra.stride_a = (int64_t)P.M[1] * P.H; ra.stride_b = P.H; }
     ra.comp_item = ce;
