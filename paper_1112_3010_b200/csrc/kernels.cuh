@@ -22,6 +22,7 @@
 // kernels are line-major (a row is contiguous in memory).
 #pragma once
 #include "fft_core.cuh"
+#include "tmem.cuh"
 
 namespace eik {
 
@@ -284,6 +285,71 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       }
     }
   }
+}
+
+// Column pass, distance group, with the forward spectrum parked in TMEM.
+// Same arithmetic as col_kernel<L, IN, OUT_COMPS, HALF> (bit-identical
+// results); E = 16, 256+ threads, two CTAs per SM.
+template <int L>
+struct TmCfg {
+  using LN = Line<L, 16>;
+  static constexpr int NT = LN::TPL > 256 ? LN::TPL : 256;
+  static constexpr int LPC = NT / LN::TPL;
+  static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread
+  static constexpr int NEED = (NT / 128) * WPT;
+  static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ) * sizeof(double2) + 16;
+};
+
+template <int L, int IN, bool HALF>
+__global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_constant__ ColArgs a) {
+  using TC = TmCfg<L>;
+  using LN = typename TC::LN;
+  constexpr int LPC = TC::LPC;
+  extern __shared__ double2 smem[];
+  const int line = threadIdx.x % LPC;
+  const int t = threadIdx.x / LPC;
+  const int64_t l = (int64_t)blockIdx.x * LPC + line;
+  const bool valid = l < a.nlines;
+  const int64_t item = blockIdx.y;
+  XBuf<1> xb{smem + line * LN::SMEM, nullptr, 0};
+  double2* twq = smem + LPC * LN::SMEM;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(twq + LN::TWQ);
+  if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
+  const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle table
+  const uint32_t ta = tmem_thread_addr(tbase, TC::WPT);
+
+  double2 v[LN::EPT];
+  if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
+  else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
+  fft_line<LN, false, HALF>(v, t, xb, twq, L);
+  tmem_put(ta, v);
+  double kn[LN::EPT];
+  if (valid) {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[0], l, LN::out_idx(t, r), LN::M);
+  }
+#pragma unroll 1
+  for (int j = 0; j < a.n_comp; ++j) {
+    tmem_get(ta, v);
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) v[r] = kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M);
+      if (j + 1 < a.n_comp) {
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[j + 1], l, LN::out_idx(t, r), LN::M);
+      }
+    }
+    fft_line<LN, true>(v, t, xb, twq, L);
+    double2* dst = a.out[j] + item * a.out_item + l;
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) {
+      if (LN::L > 0 && LN::upper_in(r)) continue;
+      const int n = LN::in_idx(t, r);
+      if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = v[r];
+    }
+  }
+  tmem_free_cta(tbase, TC::COLS);
 }
 
 // Strided batched c2c lines (3D axis 1, both directions).  Line l of component

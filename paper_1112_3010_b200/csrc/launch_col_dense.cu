@@ -1,7 +1,34 @@
+#include <cstdlib>
+
 #include "launch.cuh"
+
+// EIK_TMEM=0 selects the register-resident column kernel for A/B runs.
+static bool use_tmem() {
+  static const bool on = [] {
+    const char* e = std::getenv("EIK_TMEM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int L, int IN, bool HALF>
+int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
+  using C = TmCfg<L>;
+  auto k = col_tmem_kernel<L, IN, HALF>;
+  CK(prep_kernel_attr(k, C::SMEM_BYTES));
+  const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
+  if (tiles <= 0 || items <= 0) return EIK_OK;
+  if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
+  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);
+  CK(cudaGetLastError());
+  return EIK_OK;
+}
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
+  if constexpr (OUT == OUT_COMPS && L >= 9) {
+    if (use_tmem() && a.ks[0].cplx == nullptr) return launch_tmem_t<L, IN, HALF>(a, items, st);
+  }
   using C = ColCfg<L>;
   auto k = col_kernel<L, IN, OUT, HALF>;
   const size_t smem = C::SMEM_BYTES + (IN == IN_SPARSE ? SPARSE_SMEM : 0);
