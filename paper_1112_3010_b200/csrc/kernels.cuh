@@ -301,7 +301,7 @@ struct TmCfg {
   static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ) * sizeof(double2) + 16;
 };
 
-template <int L, int IN, bool HALF>
+template <int L, int IN, int OUT, bool HALF>
 __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_constant__ ColArgs a) {
   using TC = TmCfg<L>;
   using LN = typename TC::LN;
@@ -320,6 +320,40 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
   const uint32_t ta = tmem_thread_addr(tbase, TC::WPT);
 
   double2 v[LN::EPT];
+  if constexpr (OUT == OUT_SUM) {
+    // y = sum_i K_i X_i accumulated in TMEM while each input is transformed in registers
+#pragma unroll 1
+    for (int i = 0; i < a.n_in; ++i) {
+      double kn[LN::EPT];
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[i], l, LN::out_idx(t, r), LN::M);
+      }
+      if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
+      else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+      fft_line<LN, false, HALF>(v, t, xb, twq, L);
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r)
+        v[r] = valid ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M) : make_double2(0.0, 0.0);
+      if (i > 0) {
+        double2 y[LN::EPT];
+        tmem_get(ta, y);
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r) v[r] = cadd(y[r], v[r]);
+      }
+      if (i + 1 < a.n_in) tmem_put(ta, v);
+    }
+    fft_line<LN, true>(v, t, xb, twq, L);
+    double2* dst = a.out[0] + item * a.out_item + l;
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) {
+      if (LN::L > 0 && LN::upper_in(r)) continue;
+      const int n = LN::in_idx(t, r);
+      if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = v[r];
+    }
+    tmem_free_cta(tbase, TC::COLS);
+    return;
+  }
   if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
   else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
   fft_line<LN, false, HALF>(v, t, xb, twq, L);
@@ -604,7 +638,7 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
 }
 
 template <int LH>
-__global__ void __launch_bounds__(RowCfg<LH>::NT) row_kernel(const __grid_constant__ RowArgs a) {
+__global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 1) row_kernel(const __grid_constant__ RowArgs a) {
   using LN = typename RowCfg<LH>::LN;
   constexpr int LPC = RowCfg<LH>::LPC;
   constexpr int E = LN::EPT;

@@ -11,10 +11,10 @@ static bool use_tmem() {
   return on;
 }
 
-template <int L, int IN, bool HALF>
+template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
   using C = TmCfg<L>;
-  auto k = col_tmem_kernel<L, IN, HALF>;
+  auto k = col_tmem_kernel<L, IN, OUT, HALF>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
   if (tiles <= 0 || items <= 0) return EIK_OK;
@@ -26,8 +26,8 @@ int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
-  if constexpr (OUT == OUT_COMPS && L >= 9) {
-    if (use_tmem() && a.ks[0].cplx == nullptr) return launch_tmem_t<L, IN, HALF>(a, items, st);
+  if constexpr ((OUT == OUT_COMPS || OUT == OUT_SUM) && L >= 9) {
+    if (use_tmem() && a.ks[0].cplx == nullptr) return launch_tmem_t<L, IN, OUT, HALF>(a, items, st);
   }
   using C = ColCfg<L>;
   auto k = col_kernel<L, IN, OUT, HALF>;
