@@ -179,7 +179,88 @@ struct Line {
   }
   // register i is a structurally-zero input of a half-padded forward transform
   __device__ static __forceinline__ constexpr bool upper_in(int i) { return (i % R0) >= (R0 / 2); }
+
+  // Per-stage twiddle tables (shared memory).  Stage (NS, R) needs
+  // W_{NS*R}^{k*r}, k < NS, 1 <= r < R.  With k = 16*k_hi + k_lo the table
+  // holds lo[k_lo][r] = W^{k_lo*r} and hi[k_hi][r] = W^{16*k_hi*r}; a twiddle
+  // is lo * hi (one product) or lo alone when NS <= 16.  Consecutive threads
+  // differ in k_lo and read rows R-1 entries apart (odd stride: no bank
+  // conflicts); k_hi is shared by 16 threads (broadcast).  The inverse
+  // schedule reuses the forward tables when it has the same stage types.
+  static constexpr bool INV_SHARES = (R0 == E);
+  __host__ __device__ static constexpr int st_lo(bool inv, int s) { return ns(inv, s) < 16 ? ns(inv, s) : 16; }
+  // two-level (lo * hi) tables for radix <= 8 lines; radix-16 stages with NS > 16
+  // read the quarter-wave table instead (measured faster: 15 extra products per
+  // butterfly cost more than one rotated table read)
+  static constexpr bool TWO_LEVEL = (E <= 8);
+  __host__ __device__ static constexpr bool st_quarter(bool inv, int s) { return !TWO_LEVEL && ns(inv, s) > 16; }
+  __host__ __device__ static constexpr int st_hi(bool inv, int s) {
+    return (ns(inv, s) > 16 && TWO_LEVEL) ? ns(inv, s) / 16 : 0;
+  }
+  __host__ __device__ static constexpr int st_size(bool inv, int s) {
+    return (s == 0 || st_quarter(inv, s)) ? 0 : (st_lo(inv, s) + st_hi(inv, s)) * (rad(inv, s) - 1);
+  }
+  __host__ __device__ static constexpr int st_off(bool inv, int s) {
+    int o = 0;
+    if (inv && INV_SHARES) inv = false;
+    if (inv)
+      for (int j = 1; j < NST; ++j) o += st_size(false, j);
+    for (int j = 1; j < s; ++j) o += st_size(inv, j);
+    return o;
+  }
+  __host__ __device__ static constexpr int st_total() {
+    int o = 0;
+    for (int j = 1; j < NST; ++j) o += st_size(false, j) + (INV_SHARES ? 0 : st_size(true, j));
+    return o < 1 ? 1 : o;
+  }
+  static constexpr int ST_SIZE = st_total();  // double2 slots of all stage tables
 };
+
+// Fill the stage tables of line type LN from the global table W_MAX^j.
+template <class LN, bool INV, int S>
+__device__ __forceinline__ void st_fill_stage(double2* sts, const double2* __restrict__ gtw, int lmax) {
+  if constexpr (S < LN::NST) {
+    if constexpr (S >= 1 && !(INV && LN::INV_SHARES)) {
+      constexpr int NS = LN::ns(INV, S), R = LN::rad(INV, S);
+      constexpr int NLO = LN::st_lo(INV, S), SZ = LN::st_size(INV, S), OFF = LN::st_off(INV, S);
+      const int sh = lmax - ilog2c(NS * R);
+      for (int i = threadIdx.x; i < SZ; i += blockDim.x) {
+        const int row = i / (R - 1), r = i % (R - 1) + 1;
+        const int m = row < NLO ? row * r : 16 * (row - NLO) * r;
+        sts[OFF + i] = __ldg(gtw + ((int64_t)m << sh));
+      }
+    }
+    st_fill_stage<LN, INV, S + 1>(sts, gtw, lmax);
+  }
+}
+template <class LN>
+__device__ __forceinline__ void st_fill(double2* sts, const double2* __restrict__ gtw, int lmax) {
+  st_fill_stage<LN, false, 0>(sts, gtw, lmax);
+  st_fill_stage<LN, true, 0>(sts, gtw, lmax);
+}
+
+// Twiddle sources of a line: stage tables + the quarter-wave table (resolution 2^lq >= M).
+struct TwSrc {
+  const double2* st;
+  const double2* q;
+  int lq;
+};
+
+template <class LN, bool INV, int S>
+__device__ __forceinline__ double2 st_tw(const TwSrc& tw, int k, int r) {
+  constexpr int NS = LN::ns(INV, S), R = LN::rad(INV, S);
+  constexpr int NLO = LN::st_lo(INV, S), OFF = LN::st_off(INV, S);
+  const double2* sts = tw.st;
+  if constexpr (LN::st_quarter(INV, S)) {
+    return twq_get(tw.q, tw.lq, (k * r) << (tw.lq - ilog2c(NS * R)));
+  } else if constexpr (NS <= 16) {
+    return sts[OFF + k * (R - 1) + (r - 1)];
+  } else {
+    const double2 lo = sts[OFF + (k & 15) * (R - 1) + (r - 1)];
+    const double2 hi = sts[OFF + (NLO + (k >> 4)) * (R - 1) + (r - 1)];
+    return cmul(lo, hi);
+  }
+}
 
 // Exchange buffers of one line.  With NBUF = 2 consecutive exchanges alternate
 // between two buffers, so a stage needs one __syncthreads (between its writes
@@ -201,7 +282,7 @@ struct XBuf {
 // shared-memory exchange into the next stage's register layout.
 // twq: shared quarter table at resolution 2^lq (lq >= L).
 template <class LN, bool INV, int S, bool HALF_IN, class XB>
-__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, const double2* twq, int lq) {
+__device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw) {
   constexpr int R = LN::rad(INV, S);
   constexpr int NS = LN::ns(INV, S);
   constexpr int G = LN::EPT / R;
@@ -210,10 +291,9 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
     const int b = t + g * LN::TPL;
     if constexpr (NS > 1) {
       const int k = b & (NS - 1);
-      const int sh = lq - ilog2c(NS * R);
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        const double2 w = twq_get(twq, lq, (k * r) << sh);
+        const double2 w = st_tw<LN, INV, S>(tw, k, r);
         v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
       }
     }
@@ -242,19 +322,19 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
 }
 
 template <class LN, bool INV, int S, bool HALF_IN, class XB>
-__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, XB& xb, const double2* twq, int lq) {
+__device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw) {
   if constexpr (S < LN::NST) {
-    stage<LN, INV, S, HALF_IN>(v, t, xb, twq, lq);
-    stages_from<LN, INV, S + 1, HALF_IN>(v, t, xb, twq, lq);
+    stage<LN, INV, S, HALF_IN>(v, t, xb, tw);
+    stages_from<LN, INV, S + 1, HALF_IN>(v, t, xb, tw);
   }
 }
 
 // Full transform of the line held in v (layouts documented above).
 // HALF_IN (forward only): input elements >= M/2 are zero and their registers are not read.
 template <class LN, bool INV, bool HALF_IN = false, class XB>
-__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const double2* twq, int lq) {
+__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw) {
   static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
-  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, twq, lq);
+  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, tw);
 }
 
 }  // namespace eik

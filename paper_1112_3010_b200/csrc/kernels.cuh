@@ -51,7 +51,7 @@ struct ColCfg {
   // they were measured to pay off without costing occupancy (C5-sized lines)
   static constexpr int NBUF = ((L == 10 || L == 11) && (2 * LPC * LN::SMEM + LN::TWQ) * 16 <= 200 * 1024) ? 2 : 1;
   using XB = XBuf<NBUF>;
-  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + LN::TWQ) * sizeof(double2);
+  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
 };
 // Row kernels (c2r / r2c along the contiguous last axis): complex lines of
 // length 2^LH = M_last/2, quarter table at the resolution of M_last.
@@ -64,7 +64,7 @@ struct RowCfg {
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
   static constexpr int NBUF = (LH <= 10 && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
   using XB = XBuf<NBUF>;
-  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ) * sizeof(double2);
+  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
 };
 
 // Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
@@ -197,14 +197,17 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   using CC = ColCfg<L>;
   typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
+  double2* sts = twq + LN::TWQ;
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
+  st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
+  const TwSrc tws{sts, twq, L};
 
   double2 v[LN::EPT];
   if constexpr (OUT == OUT_COMPS) {
     if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
     else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
-    fft_line<LN, false, HALF>(v, t, xb, twq, L);
+    fft_line<LN, false, HALF>(v, t, xb, tws);
     const bool real_ks = a.ks[0].cplx == nullptr;
     double kn[LN::EPT];  // next component's kernel spectrum, prefetched
     if (real_ks && valid) {
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kmul(v[r], a.ks[j], l, LN::out_idx(t, r), LN::M) : v[r];
       }
-      fft_line<LN, true>(y, t, xb, twq, L);
+      fft_line<LN, true>(y, t, xb, tws);
       double2* dst = a.out[j] + item * a.out_item + l;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, xb, twq, L);
+      fft_line<LN, false, HALF>(v, t, xb, tws);
       if (valid) {
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r)
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
                                     : kmul(v[r], a.ks[i], l, LN::out_idx(t, r), LN::M));
       }
     }
-    fft_line<LN, true>(y, t, xb, twq, L);
+    fft_line<LN, true>(y, t, xb, tws);
     double2* dst = a.out[0] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     for (int i = 0; i < a.n_in; ++i) {
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, xb, twq, L);
+      fft_line<LN, false, HALF>(v, t, xb, tws);
       if (!valid) continue;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
@@ -298,7 +301,7 @@ struct TmCfg {
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread
   static constexpr int NEED = (NT / 128) * WPT;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ) * sizeof(double2) + 16;
+  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
 };
 
 template <int L, int IN, int OUT, bool HALF>
@@ -314,9 +317,12 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
   const int64_t item = blockIdx.y;
   XBuf<1> xb{smem + line * LN::SMEM, nullptr, 0};
   double2* twq = smem + LPC * LN::SMEM;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(twq + LN::TWQ);
+  double2* sts = twq + LN::TWQ;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sts + LN::ST_SIZE);
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
-  const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle table
+  st_fill<LN>(sts, a.tw, a.lmax);
+  const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle tables
+  const TwSrc tws{sts, twq, L};
   const uint32_t ta = tmem_thread_addr(tbase, TC::WPT);
 
   double2 v[LN::EPT];
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-      fft_line<LN, false, HALF>(v, t, xb, twq, L);
+      fft_line<LN, false, HALF>(v, t, xb, tws);
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r)
         v[r] = valid ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M) : make_double2(0.0, 0.0);
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
       }
       if (i + 1 < a.n_in) tmem_put(ta, v);
     }
-    fft_line<LN, true>(v, t, xb, twq, L);
+    fft_line<LN, true>(v, t, xb, tws);
     double2* dst = a.out[0] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
   }
   if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
   else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
-  fft_line<LN, false, HALF>(v, t, xb, twq, L);
+  fft_line<LN, false, HALF>(v, t, xb, tws);
   tmem_put(ta, v);
   double kn[LN::EPT];
   if (valid) {
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
         for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[j + 1], l, LN::out_idx(t, r), LN::M);
       }
     }
-    fft_line<LN, true>(v, t, xb, twq, L);
+    fft_line<LN, true>(v, t, xb, tws);
     double2* dst = a.out[j] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
@@ -413,8 +419,11 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   using CC = ColCfg<L>;
   typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
+  double2* sts = twq + LN::TWQ;
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
+  st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
+  const TwSrc tws{sts, twq, L};
   const int64_t o = valid ? l / a.inner : 0, q = valid ? l % a.inner : 0;
   const double2* src = a.in[c] + o * a.outer_in + q;
   double2* dst = a.out[c] + o * a.outer_out + q;
@@ -427,7 +436,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
                ? src[(int64_t)(e >> a.split_shift) * a.split_stride + (int64_t)(e & ((1 << a.split_shift) - 1)) * a.es_in]
                : make_double2(0.0, 0.0);
   }
-  fft_line<LN, INV, HALF>(v, t, xb, twq, L);
+  fft_line<LN, INV, HALF>(v, t, xb, tws);
   if (!valid) return;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
@@ -562,15 +571,18 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
   using RC = RowCfg<LH>;
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
+  double2* sts = twq + RC::TWQ;
   twq_fill(twq, LQ, tw, lmax);
+  st_fill<LN>(sts, tw, lmax);
   __syncthreads();
+  const TwSrc tws{sts, twq, LQ};
   double2 v[LN::EPT];
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
     const int m = LN::in_idx(t, r);
     v[r] = valid ? make_double2(gen_value(g, row, 2 * m), gen_value(g, row, 2 * m + 1)) : make_double2(0.0, 0.0);
   }
-  fft_line<LN, false>(v, t, xb, twq, LQ);
+  fft_line<LN, false>(v, t, xb, tws);
   // natural-order spectrum Z into shared memory (the buffer the last exchange
   // did not use), then split into X[k], k in [0, MH]
   double2* sm = xb.cur();
@@ -617,7 +629,7 @@ struct RowArgs {
 
 template <class LN, class XB>
 __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* __restrict__ X, int t,
-                                         XB& xb, const double2* twq, bool valid) {
+                                         XB& xb, const double2* twq, const double2* sts, bool valid) {
   constexpr int MH = LN::M;
   constexpr int LQ = LN::L + 1;
 #pragma unroll
@@ -634,7 +646,7 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
       z[r] = make_double2(0.0, 0.0);
     }
   }
-  fft_line<LN, true>(z, t, xb, twq, LQ);
+  fft_line<LN, true>(z, t, xb, TwSrc{sts, twq, LN::L + 1});
 }
 
 template <int LH>
@@ -651,7 +663,9 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
   using RC = RowCfg<LH>;
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
+  double2* sts = twq + RC::TWQ;
   twq_fill(twq, LH + 1, a.tw, a.lmax);
+  st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
   const int64_t rb = valid ? row % a.rows_a : 0;
   const int64_t roff = item * a.comp_item +
@@ -679,7 +693,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
   double2 z[E];
   unsigned cnt = 0;
   if (a.c_phi >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, xb, twq, valid);
+    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, xb, twq, sts, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -701,7 +715,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
   if (a.c_grad >= 0) {
 #pragma unroll 1
     for (int d = 0; d < a.ngrad; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, xb, twq, valid);
+      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, xb, twq, sts, valid);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -714,7 +728,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
   if (a.c_hess >= 0) {
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, xb, twq, valid);
+      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, xb, twq, sts, valid);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -728,7 +742,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
     }
   }
   if (a.c_sign >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, xb, twq, valid);
+    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, xb, twq, sts, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -750,7 +764,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
   }
 #pragma unroll 1
   for (int j = 0; j < a.n_raw; ++j) {
-    c2r_line<LN>(z, a.comp[j] + roff, t, xb, twq, valid);
+    c2r_line<LN>(z, a.comp[j] + roff, t, xb, twq, sts, valid);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
