@@ -293,16 +293,24 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    # per-pass device times (passes serialised, events between them), untimed
     pass_ms = {}
+    for i in range(max(3, min(a.steps, 10))):
+        flush.fill_(float(i))
+        step(profile=True)
+        for k, v in plan.pass_times().items():
+            pass_ms.setdefault(k, []).append(v)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     with ClockSampler(local) as clk:
         for i in range(a.steps):
             flush.fill_(float(i))  # evict L2 between timed steps (outside the events)
             ev[i][0].record(stream)
-            step(profile=True)
+            step()
             ev[i][1].record(stream)
-            for k, v in plan.pass_times().items():
-                pass_ms.setdefault(k, []).append(v)
         torch.cuda.synchronize()
     total_ms = sum(s.elapsed_time(e) for s, e in ev)
     if dist:

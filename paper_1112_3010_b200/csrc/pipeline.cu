@@ -121,9 +121,16 @@ struct eik_plan {
   std::mutex mu;
   cudaEvent_t ev[2 * EIK_NPASS] = {};
   bool ev_used[EIK_NPASS] = {};
+  // side stream: the 2-D sign group runs concurrently with the distance group
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevBuf serr;
   ~eik_plan() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (st2) cudaStreamDestroy(st2);
   }
 
   int64_t comp_elems() const {  // complex elements of one component of one item
@@ -283,17 +290,19 @@ KSpec kspec_of(const eik_plan* p, const KDev& k) {
 // per-row CSR for a sorted node list (validates order and bounds): rows of
 // length clast, rows_per_item rows and N_item nodes per item.
 int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_t K, int64_t items, int64_t N_item,
-               int64_t rows_per_item, int64_t clast, DevBuf& rowid, DevBuf& cols, DevBuf& rowptr, cudaStream_t st) {
+               int64_t rows_per_item, int64_t clast, DevBuf& rowid, DevBuf& cols, DevBuf& rowptr, cudaStream_t st,
+               DevBuf* errbuf = nullptr) {
   const int64_t nrows = rows_per_item * items;
+  DevBuf& err = errbuf ? *errbuf : p->err;
   CK(rowid.ensure(std::max<int64_t>(K, 1) * sizeof(int64_t)));
   CK(cols.ensure(std::max<int64_t>(K, 1) * sizeof(int32_t)));
   CK(rowptr.ensure((nrows + 1) * sizeof(int64_t)));
-  CK(p->err.ensure(sizeof(int)));
-  CK(cudaMemsetAsync(p->err.p, 0, sizeof(int), st));
+  CK(err.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(err.p, 0, sizeof(int), st));
   if (K > 0) {
     const int64_t per = std::max<int64_t>(1, std::min<int64_t>(1024, (K / std::max<int64_t>(items, 1) + 255) / 256));
     prep_nodes_kernel<<<dim3((unsigned)per, (unsigned)items), 256, 0, st>>>(
-        d_nodes, d_off, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), p->err.as<int>());
+        d_nodes, d_off, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), err.as<int>());
     CK(cudaGetLastError());
   }
   rowptr_kernel<<<(unsigned)((nrows + 1 + 255) / 256), 256, 0, st>>>(rowid.as<int64_t>(), K, nrows,
@@ -451,7 +460,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
   DevBuf& rid = sg ? p->srowid : p->rowid;
   DevBuf& cl = sg ? p->scols : p->cols;
   DevBuf& rp = sg ? p->srowptr : p->rowptr;
-  int rc = prep_nodes(p, nodes, off, K, B, p->N, p->c[0], p->c[1], rid, cl, rp, st);
+  int rc = prep_nodes(p, nodes, off, K, B, p->N, p->c[0], p->c[1], rid, cl, rp, st, sg ? &p->serr : nullptr);
   if (rc) return rc;
   ColArgs a = col_defaults(p);
   a.rowptr = rp.as<int64_t>();
@@ -701,16 +710,31 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
   for (int j = 0; j < n_comp; ++j) W[j] = p->comp.as<double2>() + (int64_t)j * B * ce;
   int rc;
   if (p->D == 2) {
+    // The two groups are independent column passes: run the sign group on a
+    // side stream so it fills the distance group's tail (sequential when
+    // profiling, so that per-pass times stay attributable).
+    const bool fork = want_phi && want_sign && !prof;
+    cudaStream_t ss = st;
+    if (fork) {
+      if (!p->st2) CK(cudaStreamCreateWithFlags(&p->st2, cudaStreamNonBlocking));
+      if (!p->ev_fork) CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+      if (!p->ev_join) CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+      CK(cudaEventRecord(p->ev_fork, st));
+      CK(cudaStreamWaitEvent(p->st2, p->ev_fork, 0));
+      ss = p->st2;
+    }
+    if (want_sign) {
+      if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
+      if ((rc = pass_col2d(p, true, d_snodes, p->soff.as<int64_t>(), Ks, 1, d_sw, r, W.data(), ss))) return rc;
+      if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
+    }
+    if (fork) CK(cudaEventRecord(p->ev_join, ss));
     if (want_phi) {
       if ((rc = mark(EIK_PASS_COL, false))) return rc;
       if ((rc = pass_col2d(p, false, d_nodes, d_off, in->n_nodes, B, nullptr, r, W.data(), st))) return rc;
       if ((rc = mark(EIK_PASS_COL, true))) return rc;
     }
-    if (want_sign) {
-      if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
-      if ((rc = pass_col2d(p, true, d_snodes, p->soff.as<int64_t>(), Ks, 1, d_sw, r, W.data(), st))) return rc;
-      if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
-    }
+    if (fork) CK(cudaStreamWaitEvent(st, p->ev_join, 0));
   } else {
     const int n_in_max = std::max(want_phi ? 1 : 0, want_sign ? 3 : 0);
     CK(p->vin.ensure((size_t)n_in_max * B * ce * sizeof(double2)));
@@ -751,10 +775,15 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
   int err_flag = 0;
   unsigned long long nuf = 0;
   if (sync) {
-    CK(cudaMemcpyAsync(&err_flag, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if ((want_phi || p->D == 3) && p->err.p)
+      CK(cudaMemcpyAsync(&err_flag, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int serr_flag = 0;
+    if (want_sign && p->D == 2 && p->serr.p) {
+      CK(cudaMemcpyAsync(&serr_flag, p->serr.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    }
     if (count) CK(cudaMemcpyAsync(&nuf, ctr, sizeof(nuf), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (err_flag) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
+    if (err_flag || serr_flag) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
     if (out->n_underflow) *out->n_underflow = (int64_t)nuf;
     if ((flags & EIK_CHECK_UNDERFLOW) && nuf > 0)
       return fail(EIK_EUNDERFLOW, "phi has non-positive entries after convolution; increase the precision bits "
