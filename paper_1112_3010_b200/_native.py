@@ -16,7 +16,8 @@ import numpy as np
 
 from .errors import NativeError, PrecisionError, ValidationError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libeikfld_b200.so")
+LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                     "libeikfld_b200.so")
 
 EIK_OK, EIK_EVALIDATION, EIK_EUNDERFLOW, EIK_ECUDA = 0, 1, 2, 3
 FIELD_PHI, FIELD_S, FIELD_GRAD, FIELD_HESS, FIELD_WINDING, FIELD_DEGREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20

@@ -778,6 +778,105 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
 }
 
 // ---------------------------------------------------------------------------
+// Impulse DFT along the last axis, one CTA per grid row:
+//   T_i[item][row][k] = sum_{p in row} w_i[p] W_{M_last}^{(col_p * k) mod M_last},  k in [0, H)
+// The row's points are staged in shared memory (broadcast reads), every
+// thread owns a stride of frequencies, and each T value is one thread's
+// in-order sum (bit-reproducible).  T then feeds the dense column pass; this
+// replaces the per-column re-walk of the node lists inside the column kernel.
+struct RowDftArgs {
+  const int64_t* rowptr;
+  const int32_t* cols;
+  const double* w[3];
+  int n_in;
+  int64_t rows_per_item, H;
+  double2* out[3];
+  int64_t out_item;  // complex elements per item (rows_per_item * H)
+  int last_shift, last_mask;
+  const double2* tw;
+};
+
+constexpr int ROWDFT_NT = 256;
+constexpr int ROWDFT_NF = 16;     // max frequencies per thread
+constexpr int ROWDFT_CHUNK = 256;  // staged points per row and chunk
+
+// Threads per row: enough for H frequencies at <= 16 each, power of two, <= 256.
+__host__ __device__ constexpr int rowdft_tpr(int64_t H) {
+  int t = 1;
+  while (t < 256 && (int64_t)t * ROWDFT_NF < H) t <<= 1;
+  return t;
+}
+
+template <int NIN>
+__global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_constant__ RowDftArgs a) {
+  extern __shared__ double rowdft_smem[];
+  const int tpr = rowdft_tpr(a.H);
+  const int rpb = ROWDFT_NT / tpr;
+  const int rl = threadIdx.x / tpr, tl = threadIdx.x % tpr;
+  const int64_t item = blockIdx.y;
+  const int64_t row = (int64_t)blockIdx.x * rpb + rl;
+  const bool valid = row < a.rows_per_item;
+  // per-row staging: [rpb][CHUNK] columns + [NIN][rpb][CHUNK] weights
+  int32_t* cols = reinterpret_cast<int32_t*>(rowdft_smem + NIN * rpb * ROWDFT_CHUNK);
+  double* ws = rowdft_smem;
+  const int64_t grow = item * a.rows_per_item + (valid ? row : 0);
+  const int64_t p0 = valid ? __ldg(a.rowptr + grow) : 0, p1 = valid ? __ldg(a.rowptr + grow + 1) : 0;
+  const int nk = (int)((a.H + tpr - 1) / tpr);
+  double2 acc[NIN][ROWDFT_NF];
+#pragma unroll
+  for (int i = 0; i < NIN; ++i)
+#pragma unroll
+    for (int q = 0; q < ROWDFT_NF; ++q) acc[i][q] = make_double2(0.0, 0.0);
+  // rows of one CTA may differ in length: loop to the CTA's longest row
+  __shared__ int s_maxlen;
+  if (threadIdx.x == 0) s_maxlen = 0;
+  __syncthreads();
+  if (tl == 0) atomicMax(&s_maxlen, (int)(p1 - p0));
+  __syncthreads();
+  const int maxlen = s_maxlen;
+  for (int cs = 0; cs < maxlen; cs += ROWDFT_CHUNK) {
+    const int64_t left = p1 - p0 - cs;
+    const int n = left <= 0 ? 0 : (left < ROWDFT_CHUNK ? (int)left : ROWDFT_CHUNK);
+    __syncthreads();
+    for (int q = tl; q < n; q += tpr) {
+      cols[rl * ROWDFT_CHUNK + q] = __ldg(a.cols + p0 + cs + q);
+#pragma unroll
+      for (int i = 0; i < NIN; ++i)
+        ws[(i * rpb + rl) * ROWDFT_CHUNK + q] = a.w[i] ? __ldg(a.w[i] + p0 + cs + q) : 1.0;
+    }
+    __syncthreads();
+    for (int p = 0; p < n; ++p) {
+      const int64_t col = cols[rl * ROWDFT_CHUNK + p];
+      double wv[NIN];
+#pragma unroll
+      for (int i = 0; i < NIN; ++i) wv[i] = ws[(i * rpb + rl) * ROWDFT_CHUNK + p];
+#pragma unroll
+      for (int q = 0; q < ROWDFT_NF; ++q) {
+        const int64_t k = tl + (int64_t)q * tpr;
+        if (q < nk && k < a.H) {
+          const double2 t = __ldg(a.tw + ((int)((col * k) & a.last_mask) << a.last_shift));
+#pragma unroll
+          for (int i = 0; i < NIN; ++i) {
+            acc[i][q].x = fma(wv[i], t.x, acc[i][q].x);
+            acc[i][q].y = fma(wv[i], t.y, acc[i][q].y);
+          }
+        }
+      }
+    }
+  }
+  if (!valid) return;
+#pragma unroll
+  for (int i = 0; i < NIN; ++i) {
+    double2* dst = a.out[i] + item * a.out_item + row * a.H;
+#pragma unroll
+    for (int q = 0; q < ROWDFT_NF; ++q) {
+      const int64_t k = tl + (int64_t)q * tpr;
+      if (q < nk && k < a.H) dst[k] = acc[i][q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Node-list preparation: validation + per-row CSR, deterministic.
 
 static __global__ void prep_nodes_kernel(const int64_t* __restrict__ nodes, const int64_t* __restrict__ item_off,

@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -124,7 +125,7 @@ struct eik_plan {
   // side stream: the 2-D sign group runs concurrently with the distance group
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  DevBuf serr;
+  DevBuf serr, trows, tsign;
   ~eik_plan() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -137,7 +138,7 @@ struct eik_plan {
     return D == 2 ? (int64_t)c[0] * H : (int64_t)c[0] * M[1] * H;
   }
   int64_t held() const {
-    int64_t b = tw.bytes + comp.bytes + vin.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
+    int64_t b = tw.bytes + comp.bytes + vin.bytes + trows.bytes + tsign.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
                 scols.bytes + srowptr.bytes + stage.bytes + work.bytes + h_nodes.bytes + h_off.bytes +
                 h_snodes.bytes + h_sw.bytes;
     for (auto& k : kdist) b += k->buf.bytes;
@@ -462,6 +463,55 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
   DevBuf& rp = sg ? p->srowptr : p->rowptr;
   int rc = prep_nodes(p, nodes, off, K, B, p->N, p->c[0], p->c[1], rid, cl, rp, st, sg ? &p->serr : nullptr);
   if (rc) return rc;
+  const int n_in = sg ? p->dim : 1;
+  // Sparse inputs (the BASELINE configs: K << N) go through the row-DFT pass
+  // into a dense T[row][k1] and the dense column kernel; EIK_ROWDFT=0 keeps the
+  // node-list walk inside the column kernel.
+  static const bool rowdft = [] {
+    const char* e = std::getenv("EIK_ROWDFT");
+    return !(e && e[0] == '0');
+  }();
+  if (rowdft && p->H <= (int64_t)ROWDFT_NF * ROWDFT_NT) {
+    DevBuf& T = sg ? p->tsign : p->trows;
+    const int64_t per = (int64_t)p->c[0] * p->H;
+    CK(T.ensure((size_t)n_in * B * per * sizeof(double2)));
+    RowDftArgs ra{};
+    ra.rowptr = rp.as<int64_t>();
+    ra.cols = cl.as<int32_t>();
+    ra.n_in = n_in;
+    for (int i = 0; i < 3; ++i) {
+      ra.w[i] = (sg && i < n_in) ? w + (int64_t)i * K : nullptr;
+      ra.out[i] = i < n_in ? T.as<double2>() + (int64_t)i * B * per : nullptr;
+    }
+    ra.rows_per_item = p->c[0];
+    ra.H = p->H;
+    ra.out_item = per;
+    ra.last_shift = p->lmax - p->L[1];
+    ra.last_mask = p->M[1] - 1;
+    ra.tw = p->tw.as<double2>();
+    {
+      const int tpr = rowdft_tpr(p->H), rpb = ROWDFT_NT / tpr;
+      const size_t smem = (size_t)rpb * ROWDFT_CHUNK * (n_in * sizeof(double) + sizeof(int32_t));
+      const dim3 grid((unsigned)((p->c[0] + rpb - 1) / rpb), (unsigned)B);
+      if (n_in == 1) impulse_rows_kernel<1><<<grid, ROWDFT_NT, smem, st>>>(ra);
+      else if (n_in == 2) impulse_rows_kernel<2><<<grid, ROWDFT_NT, smem, st>>>(ra);
+      else impulse_rows_kernel<3><<<grid, ROWDFT_NT, smem, st>>>(ra);
+      CK(cudaGetLastError());
+    }
+    ColArgs a = col_defaults(p);
+    a.nlines = p->H;
+    a.n_valid = p->c[0];
+    a.n_out = p->c[0];
+    a.n_in = n_in;
+    for (int i = 0; i < n_in; ++i) a.din[i] = ra.out[i];
+    a.din_es = p->H;
+    a.din_item = per;
+    a.out_es = p->H;
+    a.out_item = p->comp_elems();
+    set_components(p, sg, r, a, W, 0);
+    return sg ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st)
+              : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st);
+  }
   ColArgs a = col_defaults(p);
   a.rowptr = rp.as<int64_t>();
   a.cols = cl.as<int32_t>();
