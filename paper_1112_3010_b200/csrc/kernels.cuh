@@ -398,8 +398,9 @@ struct LinesArgs {
   const double2* in[MAXC];
   double2* out[MAXC];
   int64_t nlines, inner, outer_in, outer_out, es_in, es_out;
-  int split_shift;              // element e -> (e >> shift) * split_stride + (e & (2^shift - 1)) * es
-  int64_t split_stride;
+  // element e -> (e >> shift) * split_stride + (e & (2^shift - 1)) * es, separately for in / out
+  int split_shift, split_shift_out;
+  int64_t split_stride, split_stride_out;
   int n_valid, n_out;
   double scale;
   const double2* tw;
@@ -444,7 +445,8 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
     if (n < a.n_out) {
       double2 x = v[r];
       if (a.scale != 1.0) { x.x *= a.scale; x.y *= a.scale; }
-      dst[(int64_t)(n >> a.split_shift) * a.split_stride + (int64_t)(n & ((1 << a.split_shift) - 1)) * a.es_out] = x;
+      dst[(int64_t)(n >> a.split_shift_out) * a.split_stride_out +
+          (int64_t)(n & ((1 << a.split_shift_out) - 1)) * a.es_out] = x;
     }
   }
 }
@@ -798,7 +800,7 @@ struct RowDftArgs {
 
 constexpr int ROWDFT_NT = 256;
 constexpr int ROWDFT_NF = 16;     // max frequencies per thread
-constexpr int ROWDFT_CHUNK = 256;  // staged points per row and chunk
+constexpr int ROWDFT_STAGE = 1536;  // staged points per CTA and chunk (<= 42 KB of shared memory)
 
 // Threads per row: enough for H frequencies at <= 16 each, power of two, <= 256.
 __host__ __device__ constexpr int rowdft_tpr(int64_t H) {
@@ -813,6 +815,7 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   const int tpr = rowdft_tpr(a.H);
   const int rpb = ROWDFT_NT / tpr;
   const int rl = threadIdx.x / tpr, tl = threadIdx.x % tpr;
+  const int ROWDFT_CHUNK = ROWDFT_STAGE / rpb;  // per row
   const int64_t item = blockIdx.y;
   const int64_t row = (int64_t)blockIdx.x * rpb + rl;
   const bool valid = row < a.rows_per_item;

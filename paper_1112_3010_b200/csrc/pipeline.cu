@@ -161,8 +161,8 @@ ColArgs col_defaults(const eik_plan* p) {
 }
 LinesArgs lines_defaults(const eik_plan* p) {
   LinesArgs la{};
-  la.split_shift = NOSPLIT;
-  la.split_stride = 0;
+  la.split_shift = la.split_shift_out = NOSPLIT;
+  la.split_stride = la.split_stride_out = 0;
   la.scale = 1.0;
   la.tw = p->tw.as<double2>();
   la.lmax = p->lmax;
@@ -491,7 +491,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     ra.tw = p->tw.as<double2>();
     {
       const int tpr = rowdft_tpr(p->H), rpb = ROWDFT_NT / tpr;
-      const size_t smem = (size_t)rpb * ROWDFT_CHUNK * (n_in * sizeof(double) + sizeof(int32_t));
+      const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
       const dim3 grid((unsigned)((p->c[0] + rpb - 1) / rpb), (unsigned)B);
       if (n_in == 1) impulse_rows_kernel<1><<<grid, ROWDFT_NT, smem, st>>>(ra);
       else if (n_in == 2) impulse_rows_kernel<2><<<grid, ROWDFT_NT, smem, st>>>(ra);
@@ -541,6 +541,52 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
   DevBuf& rp = sg ? p->srowptr : p->rowptr;
   int rc = prep_nodes(p, nodes, off, K, B, c0loc * c1 * c2, c0loc * c1, c2, rid, cl, rp, st);
   if (rc) return rc;
+  const int n_in = sg ? 3 : 1;
+  static const bool rowdft = [] {
+    const char* e = std::getenv("EIK_ROWDFT");
+    return !(e && e[0] == '0');
+  }();
+  if (rowdft && H <= (int64_t)ROWDFT_NF * ROWDFT_NT) {
+    // impulse DFT along axis 2 per row (i0, i1) into T[i0][i1][k2], then a dense
+    // (half-padded) FFT along axis 1 straight into the packed V layout
+    DevBuf& T = p->trows;
+    const int64_t per = c0loc * c1 * H;
+    CK(T.ensure((size_t)n_in * B * per * sizeof(double2)));
+    RowDftArgs ra{};
+    ra.rowptr = rp.as<int64_t>();
+    ra.cols = cl.as<int32_t>();
+    ra.n_in = n_in;
+    for (int i = 0; i < 3; ++i) {
+      ra.w[i] = (sg && i < n_in) ? w + (int64_t)i * K : nullptr;
+      ra.out[i] = i < n_in ? T.as<double2>() + (int64_t)i * B * per : nullptr;
+    }
+    ra.rows_per_item = c0loc * c1;
+    ra.H = H;
+    ra.out_item = per;
+    ra.last_shift = p->lmax - p->L[2];
+    ra.last_mask = p->M[2] - 1;
+    ra.tw = p->tw.as<double2>();
+    const int tpr = rowdft_tpr(H), rpb = ROWDFT_NT / tpr;
+    const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
+    const dim3 grid((unsigned)((c0loc * c1 + rpb - 1) / rpb), (unsigned)B);
+    if (n_in == 1) impulse_rows_kernel<1><<<grid, ROWDFT_NT, smem, st>>>(ra);
+    else impulse_rows_kernel<3><<<grid, ROWDFT_NT, smem, st>>>(ra);
+    CK(cudaGetLastError());
+    LinesArgs la = lines_defaults(p);
+    for (int i = 0; i < n_in; ++i) { la.in[i] = ra.out[i]; la.out[i] = V[i]; }
+    la.nlines = B * c0loc * H;
+    la.inner = H;
+    la.outer_in = c1 * H;
+    la.outer_out = ks * H;
+    la.es_in = la.es_out = H;
+    if (ks < p->M[1]) {
+      la.split_shift_out = ilog2_exact(ks);
+      la.split_stride_out = c0loc * ks * H;
+    }
+    la.n_valid = (int)c1;
+    la.n_out = p->M[1];
+    return launch_lines<false, true>(p->L[1], la, n_in, st);
+  }
   ColArgs a = col_defaults(p);
   a.rowptr = rp.as<int64_t>();
   a.cols = cl.as<int32_t>();
@@ -600,8 +646,8 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
     la.outer_in = la.outer_out = ks * H;
     la.es_in = la.es_out = H;
     if (ks < p->M[1]) {
-      la.split_shift = ilog2_exact(ks);
-      la.split_stride = c0loc * ks * H;
+      la.split_shift = la.split_shift_out = ilog2_exact(ks);
+      la.split_stride = la.split_stride_out = c0loc * ks * H;
     }
     la.n_valid = p->M[1];
     la.n_out = p->c[1];
