@@ -17,7 +17,7 @@ from paper_1112_3010_b200 import _native, sign, workloads
 
 def header_symbols():
     text = open(os.path.join(REPO, "include", "eikfld_b200.h")).read()
-    return sorted(set(re.findall(r"\b(eik_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(eik_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_header_symbols():
