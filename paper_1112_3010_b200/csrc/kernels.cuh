@@ -607,6 +607,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
 
 struct RowArgs {
   int64_t rows;        // rows per item
+  int64_t row0, row_end, item0;  // this launch covers rows [row0, row_end) of items item0 + blockIdx.y
   int n_out;           // grid count along the last axis
   int64_t rows_a, stride_a, stride_b, comp_item;  // row -> (row / rows_a)*stride_a + b(row % rows_a)
   int split_shift;                                 // b(x) = (x >> shift)*split_stride + (x & (2^shift-1))*stride_b
@@ -659,9 +660,9 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
   extern __shared__ double2 smem[];
   const int line = threadIdx.x / LN::TPL;
   const int t = threadIdx.x % LN::TPL;
-  const int64_t row = (int64_t)blockIdx.x * LPC + line;
-  const bool valid = row < a.rows;
-  const int64_t item = blockIdx.y;
+  const int64_t row = a.row0 + (int64_t)blockIdx.x * LPC + line;
+  const bool valid = row < a.row_end;
+  const int64_t item = a.item0 + blockIdx.y;
   using RC = RowCfg<LH>;
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;

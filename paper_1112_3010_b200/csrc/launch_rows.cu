@@ -5,7 +5,7 @@ int launch_row_t(const RowArgs& a, int64_t items, cudaStream_t st) {
   using C = RowCfg<LH>;
   auto k = row_kernel<LH>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
-  const int64_t tiles = (a.rows + C::LPC - 1) / C::LPC;
+  const int64_t tiles = (a.row_end - a.row0 + C::LPC - 1) / C::LPC;
   if (tiles <= 0) return EIK_OK;
   if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
   k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);

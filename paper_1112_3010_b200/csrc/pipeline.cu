@@ -123,8 +123,8 @@ struct eik_plan {
   cudaEvent_t ev[2 * EIK_NPASS] = {};
   bool ev_used[EIK_NPASS] = {};
   // side stream: the 2-D sign group runs concurrently with the distance group
-  cudaStream_t st2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t st2 = nullptr, st_copy = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr;
   DevBuf serr, trows, tsign;
   ~eik_plan() {
     for (auto& e : ev)
@@ -132,6 +132,8 @@ struct eik_plan {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
+    if (st_copy) cudaStreamDestroy(st_copy);
+    if (ev_chunk) cudaEventDestroy(ev_chunk);
   }
 
   int64_t comp_elems() const {  // complex elements of one component of one item
@@ -633,8 +635,14 @@ int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks,
 // 3-D pass C (or the 2-D row pass): inverse along axis 1 (3-D only) + c2r along
 // the last axis + epilogue, for planes [0, c0loc).  W_j laid out as
 // [k1 / ks][i0][k1 % ks][k2] (3-D) or [row][k1] (2-D).
+// on_chunk(row0, row1, item0, item1), when given, splits the row pass into
+// chunks and is called after each chunk is queued (host copies overlap the
+// remaining chunks).
+using ChunkFn = std::function<int(int64_t, int64_t, int64_t, int64_t)>;
+
 int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, int64_t ks, int64_t B,
-                RowArgs ra, cudaStream_t st, const std::function<int(int, bool)>& mark) {
+                RowArgs ra, cudaStream_t st, const std::function<int(int, bool)>& mark,
+                const ChunkFn& on_chunk = nullptr) {
   const int64_t H = p->H;
   const int nc = r.n_comp();
   int rc;
@@ -689,7 +697,36 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
   ra.tw = p->tw.as<double2>();
   ra.lmax = p->lmax;
   if ((rc = mark(EIK_PASS_ROW, false))) return rc;
-  if ((rc = launch_row(p->L[p->D - 1] - 1, ra, B, st))) return rc;
+  const int LH = p->L[p->D - 1] - 1;
+  if (!on_chunk) {
+    ra.row0 = 0;
+    ra.row_end = ra.rows;
+    ra.item0 = 0;
+    if ((rc = launch_row(LH, ra, B, st))) return rc;
+    return mark(EIK_PASS_ROW, true);
+  }
+  constexpr int kChunks = 8;
+  if (B >= kChunks) {  // chunk over items
+    for (int c = 0; c < kChunks; ++c) {
+      const int64_t i0 = B * c / kChunks, i1 = B * (c + 1) / kChunks;
+      if (i1 <= i0) continue;
+      ra.row0 = 0;
+      ra.row_end = ra.rows;
+      ra.item0 = i0;
+      if ((rc = launch_row(LH, ra, i1 - i0, st))) return rc;
+      if ((rc = on_chunk(0, ra.rows, i0, i1))) return rc;
+    }
+  } else {  // chunk over rows (every item)
+    for (int c = 0; c < kChunks; ++c) {
+      const int64_t r0 = ra.rows * c / kChunks, r1 = ra.rows * (c + 1) / kChunks;
+      if (r1 <= r0) continue;
+      ra.row0 = r0;
+      ra.row_end = r1;
+      ra.item0 = 0;
+      if ((rc = launch_row(LH, ra, B, st))) return rc;
+      if ((rc = on_chunk(r0, r1, 0, B))) return rc;
+    }
+  }
   return mark(EIK_PASS_ROW, true);
 }
 
@@ -864,7 +901,33 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     if (!out->d_underflow_count) CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     ra.uf_count = ctr;
   }
-  if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark))) return rc;
+  if (host_out && !slots.empty() && !prof && NB >= (int64_t(1) << 22)) {
+    // D2H of each finished chunk of rows on a copy stream, overlapping the rest
+    // of the row pass (the end-to-end path is PCIe-bound on the outputs)
+    if (!p->st_copy) CK(cudaStreamCreateWithFlags(&p->st_copy, cudaStreamNonBlocking));
+    if (!p->ev_chunk) CK(cudaEventCreateWithFlags(&p->ev_chunk, cudaEventDisableTiming));
+    const int64_t nlast = p->c[p->D - 1];
+    const int64_t item_nodes = p->N;
+    ChunkFn on_chunk = [&](int64_t r0, int64_t r1, int64_t i0, int64_t i1) -> int {
+      CK(cudaEventRecord(p->ev_chunk, st));
+      CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
+      for (auto& sl : slots) {
+        const size_t elem = sl.bytes / (size_t)NB;
+        for (int64_t it = i0; it < i1; ++it) {
+          const size_t off = ((size_t)it * item_nodes + (size_t)r0 * nlast) * elem;
+          const size_t len = (size_t)(r1 - r0) * nlast * elem;
+          CK(cudaMemcpyAsync((char*)sl.user + off, (char*)sl.dev + off, len, cudaMemcpyDeviceToHost, p->st_copy));
+        }
+      }
+      return EIK_OK;
+    };
+    if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark, on_chunk))) return rc;
+    CK(cudaEventRecord(p->ev_chunk, p->st_copy));
+    CK(cudaStreamWaitEvent(st, p->ev_chunk, 0));
+    slots.clear();
+  } else {
+    if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark))) return rc;
+  }
   // ---- copy back / sync / checks
   for (auto& s : slots) CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));
   const bool sync = host_out || (flags & (EIK_SYNC | EIK_CHECK_UNDERFLOW)) || out->n_underflow;
@@ -1099,6 +1162,9 @@ int eik_convolve(int dim, const int64_t* counts, const double* kernels, int64_t 
     ra.N = P.N;
     ra.tw = tw;
     ra.lmax = P.lmax;
+    ra.row0 = 0;
+    ra.row_end = ra.rows;
+    ra.item0 = 0;
     if ((rc = launch_row(P.L[last] - 1, ra, 1, st))) return rc;
   }
   if (host_out) CK(cudaMemcpyAsync(out, d_out, n_kernels * P.N * sizeof(double), cudaMemcpyDeviceToHost, st));
