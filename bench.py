@@ -110,54 +110,65 @@ def algorithmic_bytes(plan_info, w, batch):
 
 
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region.
+
+    NVML is polled in-process every ~1 ms (a C2 timed region is ~15 ms, far too
+    short for nvidia-smi's 100 ms loop); falls back to nvidia-smi if NVML is absent.
+    """
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop = threading.Event()
+        self.nv = None
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv, self.h = nv, h
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, self.max_mhz, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+            time.sleep(0.005)  # at least one sample before the region starts
+        except Exception:
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "none"}
+        sm = [x[0] for x in self.samples]
+        reasons = set()
+        for _, _, rs in self.samples:
+            for name, const in self.REASONS.items():
+                if rs & getattr(self.nv, const, 0):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(self.samples[0][1]), "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml"}
 
 
 # ---------------------------------------------------------------- CPU side
@@ -408,7 +419,9 @@ def main():
                "sample": f"1 step of the oracle pipeline on {a.config}" + (" (8 items)" if a.config == "C5" else "")
                          + f" ({sec:.1f} s), scipy.fft workers={cores}"}
 
-    launches_per_step = {"C1": 5, "C2": 7, "C3": 6, "C5": 5}[a.config]
+    # kernels per step: per group prep_nodes + rowptr + impulse_rows + column pass;
+    # + row pass (3-D: + axis-1 lines before/after the axis-0 pass)
+    launches_per_step = {"C1": 5, "C2": 9, "C3": 7, "C5": 5}[a.config]
     if rank == 0:
         line = {
             "metric": "grid points/sec (S+grad S+sign)", "value": value, "unit": "grid_points/s", "n_gpus": world,
@@ -521,7 +534,7 @@ def bench_c4(a):
                        "l2": "working set >> L2", "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": grid.num_nodes * ke / (e2e_ms / 1e3), "unit": "grid_points/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ke},
-            "gpu_launches": 10 * a.steps,
+            "gpu_launches": 12 * a.steps,
             "roofline": None,
             "cpu_baseline": {"value": None, "unit": "grid_points/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": "infeasible: the reference pads to 3072^3 (464 GB per complex array) and "
