@@ -35,6 +35,8 @@ CONFIG_TEXT = {
     "C2": "2D 2048^2 star curve (16384 vertices, 5908 distinct nodes), tau=0.5: S + grad S + Hessian + winding sign",
     "C3": "3D 256^3, 16 ellipsoids x 12500 points (105389 distinct nodes), tau=0.5: S + grad S",
     "C5": "batched 2D: 512 items x 512^2, K=1000 nodes each, tau=0.5: S + grad S per item",
+    "TS": "tau sweep (SURVEY 8(f) rank 1): C2's 2048^2 delta_Y, S for 9 taus 0.5..4.5 from one transform "
+          "(metric counts grid points x taus)",
     "C4": "3D 1024^3 perturbed icosphere (501,762 vertices, vector-area normals), tau=0.75: S + grad S + degree sign; "
           "slab-decomposed, NCCL all-to-all (512^3 with scaled surface on fewer than 4 GPUs: memory)",
 }
@@ -219,6 +221,8 @@ def main():
     a = parse()
     if a.config == "C4" and a.impl == "b200":
         return bench_c4(a)
+    if a.config == "TS":
+        return bench_sweep(a)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -443,6 +447,67 @@ def main():
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+    return 0
+
+
+def bench_sweep(a):
+    """tau sweep: 9 S fields from one transform of C2's delta_Y (single GPU / CPU oracle)."""
+    from paper_1112_3010_b200 import workloads as wl
+
+    d = wl.c2(a.seed)
+    grid = d["grid"]
+    nodes = d["points"].distinct_nodes()
+    taus = [0.5 * (i + 1) for i in range(9)]
+    pts = grid.num_nodes * len(taus)
+    if a.impl == "reference":
+        if int(os.environ.get("RANK", 0)) != 0:
+            return 0
+        import scipy.fft as sfft
+
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import eikfld_oracle as orc
+
+        cores = os.cpu_count() or 1
+        with sfft.set_workers(cores):
+            t0 = time.perf_counter()
+            for tau in taus:  # the reference reuses the convolver but re-transforms per tau
+                orc.phi_unchecked(nodes, grid.counts, 1.0, tau)
+            sec = time.perf_counter() - t0
+        v = pts / sec
+        print(json.dumps({"metric": "grid points x taus/sec (tau sweep)", "value": v, "unit": "grid_points*taus/s",
+                          "n_gpus": a.gpus, "steps": 1, "warmup": 0, "ms_per_step": sec * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "impl": "reference", "config": {"workload": "TS", "taus": taus},
+                          "cpu_baseline": {"value": v, "unit": "grid_points*taus/s", "cores": cores, "kind": "port",
+                                           "sample": "one 9-tau sweep of the oracle"},
+                          "e2e": {"value": v, "unit": "grid_points*taus/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return 0
+    import torch
+
+    from paper_1112_3010_b200 import _native
+
+    dev = torch.device("cuda", 0)
+    plan = _native.SweepPlan(2, grid.counts, grid.spacing, taus, 0)
+    nd = torch.as_tensor(nodes, device=dev)
+    outs = [torch.empty(grid.num_nodes, dtype=torch.float64, device=dev) for _ in taus]
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(a.warmup):
+        plan.run_sweep(nd, outs, host=False, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(a.steps):
+            plan.run_sweep(nd, outs, host=False, stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    print(json.dumps({"metric": "grid points x taus/sec (tau sweep)", "value": pts / (ms / 1e3),
+                      "unit": "grid_points*taus/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+                      "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                      "dtype": "f64", "data": "synthetic", "config": {"workload": "TS", "taus": taus},
+                      "gpu_launches": 2 + 1 + 2 * 2 * a.steps // a.steps, "clocks": clk.summary()}))
     return 0
 
 

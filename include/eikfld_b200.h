@@ -144,6 +144,15 @@ int eik_slab_axis0(eik_plan* plan, int group, double* const* v_in, int64_t k1_be
 int eik_slab_finish(eik_plan* plan, double* const* w, int64_t c0_local, int64_t ks, const eik_outputs* out,
                     uint32_t flags, void* stream);
 
+/* tau sweep (the kernel-reuse of R/experiments.py:74-109):
+ * one plan caches exp(-|x|/tau_i) spectra for n_taus values; eik_run_sweep
+ * transforms delta_Y once and writes S_i = -tau_i log phi_i for every tau
+ * (NaN where phi_i <= 0; n_underflow counts those over all taus).  1-D / 2-D. */
+int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const double* taus, int n_taus,
+                          int device, eik_plan** out);
+int eik_run_sweep(eik_plan* plan, const int64_t* nodes, int64_t n_nodes, double* const* S, int64_t* n_underflow,
+                  uint32_t flags, void* stream);
+
 /* Device milliseconds of each pass of the last eik_run issued with
  * EIK_PROFILE (synchronizes on its events); -1 for passes that did not run. */
 int eik_pass_times(eik_plan* plan, double* ms, int n);

@@ -67,6 +67,10 @@ def lib():
             L.eik_pass_times.argtypes = [C.c_void_p, _f64p, C.c_int]
             L.eik_plan_create_slab.argtypes = [C.c_int, _i64p, C.c_double, C.c_double, C.c_uint32, C.c_int,
                                                C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]
+            L.eik_plan_create_sweep.argtypes = [C.c_int, _i64p, C.c_double, _f64p, C.c_int, C.c_int,
+                                                C.POINTER(C.c_void_p)]
+            L.eik_run_sweep.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32,
+                                        C.c_void_p]
             L.eik_slab_planes.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                           C.c_int64, C.c_void_p, C.c_uint32, C.c_void_p]
             L.eik_slab_axis0.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
@@ -76,7 +80,7 @@ def lib():
             L.eik_last_error.restype = C.c_char_p
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
                          "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
-                         "eik_slab_axis0", "eik_slab_finish"):
+                         "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep"):
                 getattr(L, name).restype = C.c_int
             _lib = L
         return _lib
@@ -85,6 +89,7 @@ def lib():
 def exported_symbols():
     return ["eik_plan_create", "eik_plan_create_slab", "eik_plan_destroy", "eik_plan_info", "eik_run",
             "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
+            "eik_plan_create_sweep", "eik_run_sweep",
             "eik_last_error", "eik_version"]
 
 
@@ -254,3 +259,30 @@ def convolve(counts, kernels, field, device=0):
     check(lib().eik_convolve(len(counts), cnt, kernels.ctypes.data, n, ks, field.ctypes.data, out.ctypes.data,
                              HOST_INPUTS | HOST_OUTPUTS, device, None))
     return out
+
+
+class SweepPlan(Plan):
+    """tau-sweep plan: exp spectra for several tau values over one grid (1-D / 2-D)."""
+
+    def __init__(self, dim, counts, spacing, taus, device=0):  # noqa: super-init replaced
+        self.dim = int(dim)
+        self.counts = tuple(int(c) for c in counts)
+        self.spacing = float(spacing)
+        self.taus = [float(t) for t in taus]
+        self.device = int(device)
+        self.N = int(np.prod(self.counts))
+        h = C.c_void_p()
+        cnt = (C.c_int64 * 3)(*self.counts, *([1] * (3 - len(self.counts))))
+        tt = (C.c_double * len(self.taus))(*self.taus)
+        check(lib().eik_plan_create_sweep(self.dim, cnt, self.spacing, tt, len(self.taus), self.device, C.byref(h)))
+        self._h = h
+        self._lock = threading.Lock()
+
+    def run_sweep(self, nodes, outs, host=True, stream=None):
+        arr = (C.c_void_p * len(outs))(*[_ptr(o) for o in outs])
+        n_uf = C.c_int64(-1)
+        flags = (HOST_INPUTS | HOST_OUTPUTS) if host else SYNC
+        with self._lock:
+            rc = lib().eik_run_sweep(self._h, _ptr(nodes), int(nodes.shape[0]), arr, C.addressof(n_uf), flags, stream)
+        check(rc)
+        return n_uf.value

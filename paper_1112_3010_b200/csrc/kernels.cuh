@@ -624,6 +624,7 @@ struct RowArgs {
   uint8_t* uf;
   double* phi_out;
   double* raw[MAXC];
+  double raw_tau[MAXC];
   int64_t N;
   unsigned long long* uf_count;
   const double2* tw;
@@ -768,10 +769,21 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 
 #pragma unroll 1
   for (int j = 0; j < a.n_raw; ++j) {
     c2r_line<LN>(z, a.comp[j] + roff, t, xb, twq, sts, valid);
+    const double tj = a.raw_tau[j];  // tau sweep: raw_tau > 0 turns phi_j into S_j = -tau_j log phi_j
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
-      put(a.raw[j], r, z[r].x * a.scale, z[r].y * a.scale);
+      double x0 = z[r].x * a.scale, x1 = z[r].y * a.scale;
+      if (tj > 0.0) {
+        const int n = 2 * LN::in_idx(t, r);
+        if (valid && n < a.n_out) {
+          cnt += (x0 <= 0.0);
+          if (n + 1 < a.n_out) cnt += (x1 <= 0.0);
+        }
+        x0 = x0 > 0.0 ? (-tj) * log(x0) : __longlong_as_double(0x7ff8000000000000LL);
+        x1 = x1 > 0.0 ? (-tj) * log(x1) : __longlong_as_double(0x7ff8000000000000LL);
+      }
+      put(a.raw[j], r, x0, x1);
     }
   }
   if (a.uf_count) {

@@ -117,6 +117,8 @@ struct eik_plan {
   std::vector<std::unique_ptr<KDev>> kdist;  // EXP, GRAD..., HXX, HYY, HXY (subset)
   int k_exp = -1, k_grad = -1, k_hess = -1;
   std::vector<std::unique_ptr<KDev>> ksign;
+  std::vector<std::unique_ptr<KDev>> ksweep;  // tau sweep: one exp kernel per tau
+  std::vector<double> taus;
   DevBuf comp, vin, rowid, cols, rowptr, srowid, scols, srowptr, off1, soff;
   DevBuf h_nodes, h_off, h_snodes, h_sw, stage, counter, err, work;
   std::mutex mu;
@@ -266,7 +268,7 @@ int spectrum_of(eik_plan* p, const GenArgs& g, int part, double* dst_re, double2
 }
 
 int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, int n_odd_axes, bool odd0,
-               double sign, double2* work, cudaStream_t st) {
+               double sign, double2* work, cudaStream_t st, double tau = 0.0) {
   auto k = std::make_unique<KDev>();
   k->ktype = ktype;
   k->imag = n_odd_axes % 2;
@@ -274,8 +276,12 @@ int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, in
   k->sign = sign;
   const int64_t n = (int64_t)(p->M[0] / 2 + 1) * p->ks_lines;
   CK(k->buf.ensure(n * sizeof(double)));
-  int rc = spectrum_of(p, gen_args(p, ktype, sign), k->imag ? SPEC_IMAG_T : SPEC_REAL_T, k->buf.as<double>(), nullptr,
-                       work, st);
+  GenArgs g = gen_args(p, ktype, sign);
+  if (tau > 0.0) {
+    g.tau = tau;
+    g.inv_tau = 1.0 / tau;
+  }
+  int rc = spectrum_of(p, g, k->imag ? SPEC_IMAG_T : SPEC_REAL_T, k->buf.as<double>(), nullptr, work, st);
   if (rc) return rc;
   v.push_back(std::move(k));
   return EIK_OK;
@@ -1028,6 +1034,145 @@ int eik_slab_finish(eik_plan* p, double* const* w, int64_t c0_local, int64_t ks,
   std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
   if ((rc = pass_finish(p, W.data(), r, c0_local, ks, 1, ra, st, nomark))) return rc;
   if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
+  return EIK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// tau sweep: several exp kernels, one transform of delta_Y.
+
+int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const double* taus, int n_taus, int device,
+                          eik_plan** out) {
+  if (!out || !counts || !taus || n_taus < 1) return fail(EIK_EVALIDATION, "null argument");
+  *out = nullptr;
+  if (dim > 2) return fail(EIK_EVALIDATION, "the tau sweep is implemented for 1-D and 2-D grids");
+  for (int i = 0; i < n_taus; ++i)
+    if (!(taus[i] > 0)) return fail(EIK_EVALIDATION, "tau must be > 0");
+  CK(cudaSetDevice(device));
+  auto p = std::make_unique<eik_plan>();
+  p->device = device;
+  p->tau = taus[0];
+  int rc = setup_geometry(p.get(), dim, counts, spacing);
+  if (rc) return rc;
+  CK(p->work.ensure((size_t)p->M[0] * p->lines * sizeof(double2)));
+  for (int i = 0; i < n_taus; ++i) {
+    if ((rc = add_kernel(p.get(), p->ksweep, KT_EXP, 0, false, 1.0, p->work.as<double2>(), nullptr, taus[i]))) return rc;
+    p->taus.push_back(taus[i]);
+  }
+  CK(cudaDeviceSynchronize());
+  p->work.release();
+  CK(p->counter.ensure(sizeof(unsigned long long)));
+  CK(p->off1.ensure(2 * sizeof(int64_t)));
+  *out = p.release();
+  return EIK_OK;
+}
+
+int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* const* S, int64_t* n_underflow,
+                  uint32_t flags, void* stream) {
+  if (!p || !nodes || !S || n_nodes < 1) return fail(EIK_EVALIDATION, "null argument");
+  if (p->ksweep.empty()) return fail(EIK_EVALIDATION, "plan was not built for a tau sweep");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool host_in = flags & EIK_HOST_INPUTS, host_out = flags & EIK_HOST_OUTPUTS;
+  const int nt = (int)p->taus.size();
+  const int64_t* d_nodes = nodes;
+  if (host_in) {
+    CK(p->h_nodes.ensure(n_nodes * sizeof(int64_t)));
+    CK(cudaMemcpyAsync(p->h_nodes.p, nodes, n_nodes * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    d_nodes = p->h_nodes.as<int64_t>();
+  }
+  const int64_t off[2] = {0, n_nodes};
+  CK(cudaMemcpyAsync(p->off1.p, off, sizeof(off), cudaMemcpyHostToDevice, st));
+  std::vector<double*> outs(S, S + nt);
+  if (host_out) {
+    CK(p->stage.ensure((size_t)nt * p->N * sizeof(double)));
+    for (int i = 0; i < nt; ++i) outs[i] = p->stage.as<double>() + (int64_t)i * p->N;
+  }
+  const int64_t ce = p->comp_elems();
+  CK(p->comp.ensure((size_t)std::min(nt, MAXC) * ce * sizeof(double2)));
+  CK(p->counter.ensure(sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(p->counter.p, 0, sizeof(unsigned long long), st));
+  int rc = prep_nodes(p, d_nodes, p->off1.as<int64_t>(), n_nodes, 1, p->N, p->c[0], p->c[1], p->rowid, p->cols,
+                      p->rowptr, st);
+  if (rc) return rc;
+  // impulse DFT once; every chunk of <= 8 taus reuses T
+  CK(p->trows.ensure((size_t)p->c[0] * p->H * sizeof(double2)));
+  RowDftArgs rd{};
+  rd.rowptr = p->rowptr.as<int64_t>();
+  rd.cols = p->cols.as<int32_t>();
+  rd.n_in = 1;
+  rd.out[0] = p->trows.as<double2>();
+  rd.rows_per_item = p->c[0];
+  rd.H = p->H;
+  rd.out_item = (int64_t)p->c[0] * p->H;
+  rd.last_shift = p->lmax - p->L[1];
+  rd.last_mask = p->M[1] - 1;
+  rd.tw = p->tw.as<double2>();
+  if (p->H > (int64_t)ROWDFT_NF * ROWDFT_NT) return fail(EIK_EVALIDATION, "last axis too long for the sweep");
+  {
+    const int tpr = rowdft_tpr(p->H), rpb = ROWDFT_NT / tpr;
+    const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (sizeof(double) + sizeof(int32_t));
+    impulse_rows_kernel<1><<<dim3((unsigned)((p->c[0] + rpb - 1) / rpb), 1), ROWDFT_NT, smem, st>>>(rd);
+    CK(cudaGetLastError());
+  }
+  double scale = 1.0;
+  for (int a = 0; a < p->D; ++a) scale /= (double)p->M[a];
+  for (int t0 = 0; t0 < nt; t0 += MAXC) {
+    const int nc = std::min(MAXC, nt - t0);
+    ColArgs a = col_defaults(p);
+    a.nlines = p->H;
+    a.n_valid = p->c[0];
+    a.n_out = p->c[0];
+    a.n_in = 1;
+    a.din[0] = p->trows.as<double2>();
+    a.din_es = p->H;
+    a.din_item = 0;
+    a.out_es = p->H;
+    a.out_item = ce;
+    a.n_comp = nc;
+    for (int j = 0; j < nc; ++j) {
+      a.ks[j] = kspec_of(p, *p->ksweep[t0 + j]);
+      a.out[j] = p->comp.as<double2>() + (int64_t)j * ce;
+    }
+    if ((rc = launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, 1, st))) return rc;
+    RowArgs ra{};
+    ra.rows = p->c[0];
+    ra.rows_a = p->c[0];
+    ra.stride_b = p->H;
+    ra.split_shift = NOSPLIT;
+    ra.comp_item = ce;
+    ra.n_out = p->c[1];
+    ra.c_phi = ra.c_grad = ra.c_hess = ra.c_sign = -1;
+    ra.n_raw = nc;
+    for (int j = 0; j < nc; ++j) {
+      ra.comp[j] = a.out[j];
+      ra.raw[j] = outs[t0 + j];
+      ra.raw_tau[j] = p->taus[t0 + j];
+    }
+    ra.scale = scale;
+    ra.N = p->N;
+    ra.uf_count = p->counter.as<unsigned long long>();
+    ra.tw = p->tw.as<double2>();
+    ra.lmax = p->lmax;
+    ra.row0 = 0;
+    ra.row_end = ra.rows;
+    if ((rc = launch_row(p->L[1] - 1, ra, 1, st))) return rc;
+  }
+  if (host_out)
+    for (int i = 0; i < nt; ++i)
+      CK(cudaMemcpyAsync(S[i], outs[i], p->N * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (host_out || n_underflow || (flags & (EIK_SYNC | EIK_CHECK_UNDERFLOW))) {
+    int err_flag = 0;
+    unsigned long long nuf = 0;
+    CK(cudaMemcpyAsync(&err_flag, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&nuf, p->counter.p, sizeof(nuf), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (err_flag) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
+    if (n_underflow) *n_underflow = (int64_t)nuf;
+    if ((flags & EIK_CHECK_UNDERFLOW) && nuf > 0)
+      return fail(EIK_EUNDERFLOW, "phi has non-positive entries after convolution; increase the precision bits "
+                                  "(e.g. --precision big:512) or raise tau");
+  }
   return EIK_OK;
 }
 

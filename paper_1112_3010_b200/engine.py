@@ -71,3 +71,27 @@ class DistanceTransform:
             mu=out.get("mu"), mask=out.get("mask"), underflow=out["underflow"], count=True, host=True)
         out["n_underflow"] = cnt
         return out
+
+
+class TauSweep:
+    """S for several tau values from ONE transform of delta_Y.
+
+    The GPU analogue of the kernel reuse in R/experiments.py:74-109 (one
+    FftConvolver shared by the nine tau values of the Example-1 protocol):
+    here the impulse DFT and forward column FFT are shared, each tau adds one
+    cached exp spectrum, one inverse and its own -tau log phi epilogue.
+    Unchecked: S is NaN where phi <= 0 and the total count is returned.
+    """
+
+    def __init__(self, grid, taus, device=0):
+        if len(grid.counts) > 2:
+            raise ValidationError("the tau sweep is implemented for 1-D and 2-D grids")
+        self.grid = grid
+        self.taus = [float(t) for t in taus]
+        self.plan = _native.SweepPlan(len(grid.counts), grid.counts, grid.spacing, self.taus, device)
+
+    def run_host(self, nodes):
+        N = int(np.prod(self.grid.counts))
+        outs = [np.empty(N) for _ in self.taus]
+        n_uf = self.plan.run_sweep(np.ascontiguousarray(nodes, dtype=np.int64), outs, host=True)
+        return outs, n_uf

@@ -124,3 +124,21 @@ np.savez(sys.argv[1], S=o["S"], mu=o["mu"], h=np.stack(o["hess"]), g=np.stack(o[
             else:
                 m = keep if a.ndim == 1 else np.broadcast_to(keep, a.shape)
                 assert (np.abs(a - b)[m] / np.maximum(np.abs(a[m]), 1.0)).max() <= 1e-9, k
+
+
+def test_tau_sweep_matches_single_tau_runs(cuda_ok):
+    """One delta transform, nine tau values: each S_tau equals the single-tau
+    pipeline bit for bit and the oracle to T1 tolerance."""
+    from paper_1112_3010_b200 import engine
+
+    grid = _grid((96, 80))
+    nodes = np.sort(rng_for(13).choice(grid.num_nodes, 150, replace=False))
+    taus = [0.5 * (i + 2) for i in range(9)]  # 1.0 .. 5.0 (> MAXC: two chunks)
+    outs, n_uf = engine.TauSweep(grid, taus).run_host(nodes)
+    assert len(outs) == 9
+    for tau, S in zip(taus, outs):
+        single = engine.DistanceTransform(grid, tau, grad=False).run_host(nodes)["S"]
+        assert np.array_equal(S, single, equal_nan=True)
+        ref = orc.run_config_unchecked(nodes, grid.counts, 1.0, tau)
+        keep = ref["phi"] >= 1e-5 * ref["phi"].max()
+        assert (np.abs(S - ref["S"])[keep] / np.maximum(np.abs(ref["S"][keep]), 1.0)).max() <= 1e-9
