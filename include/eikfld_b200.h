@@ -153,6 +153,17 @@ int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const 
 int eik_run_sweep(eik_plan* plan, const int64_t* nodes, int64_t n_nodes, double* const* S, int64_t* n_underflow,
                   uint32_t flags, void* stream);
 
+/* Interior mask from a winding / degree field (R/sign.py:166-198): flagged
+ * nodes take mu from their nearest unflagged node with exactly the ties of
+ * scipy.ndimage.distance_transform_edt(return_indices=True) (same separable
+ * feature transform), then rint(mu) > 0 (mode 1, 2-D winding) / rint(mu) >= 1
+ * (mode 2, 3-D degree), or mu >= threshold when use_threshold.  out_mask is
+ * float64 0/1 as in the reference; with S given, out_signed = +S inside, -S
+ * outside (R/sign.py:201-208).  EIK_HOST_INPUTS|EIK_HOST_OUTPUTS for host buffers. */
+int eik_classify(int dim, const int64_t* counts, const double* mu, const int64_t* flagged_nodes, int64_t n_flagged,
+                 int mode, int use_threshold, double threshold, double* out_mask, const double* S,
+                 double* out_signed, uint32_t flags, int device, void* stream);
+
 /* Device milliseconds of each pass of the last eik_run issued with
  * EIK_PROFILE (synchronizes on its events); -1 for passes that did not run. */
 int eik_pass_times(eik_plan* plan, double* ms, int n);

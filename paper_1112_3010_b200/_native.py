@@ -71,6 +71,9 @@ def lib():
                                                 C.POINTER(C.c_void_p)]
             L.eik_run_sweep.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32,
                                         C.c_void_p]
+            L.eik_classify.argtypes = [C.c_int, _i64p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                                       C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_int,
+                                       C.c_void_p]
             L.eik_slab_planes.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                           C.c_int64, C.c_void_p, C.c_uint32, C.c_void_p]
             L.eik_slab_axis0.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
@@ -80,7 +83,8 @@ def lib():
             L.eik_last_error.restype = C.c_char_p
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
                          "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
-                         "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep"):
+                         "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep",
+                         "eik_classify"):
                 getattr(L, name).restype = C.c_int
             _lib = L
         return _lib
@@ -89,7 +93,7 @@ def lib():
 def exported_symbols():
     return ["eik_plan_create", "eik_plan_create_slab", "eik_plan_destroy", "eik_plan_info", "eik_run",
             "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
-            "eik_plan_create_sweep", "eik_run_sweep",
+            "eik_plan_create_sweep", "eik_run_sweep", "eik_classify",
             "eik_last_error", "eik_version"]
 
 
@@ -286,3 +290,23 @@ class SweepPlan(Plan):
             rc = lib().eik_run_sweep(self._h, _ptr(nodes), int(nodes.shape[0]), arr, C.addressof(n_uf), flags, stream)
         check(rc)
         return n_uf.value
+
+
+def classify(counts, mu, flagged, mode, threshold=None, S=None, device=0):
+    """GPU interior mask (float64 0/1) and, with S, the signed distance; host arrays."""
+    counts = tuple(int(c) for c in counts)
+    N = int(np.prod(counts))
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    fl = None if flagged is None else np.ascontiguousarray(flagged, dtype=np.int64)
+    mask = np.empty(N)
+    sd = None
+    if S is not None:
+        S = np.ascontiguousarray(S, dtype=np.float64)
+        sd = np.empty(N)
+    cnt = (C.c_int64 * 3)(*counts, *([1] * (3 - len(counts))))
+    check(lib().eik_classify(len(counts), cnt, mu.ctypes.data, None if fl is None else fl.ctypes.data,
+                             0 if fl is None else fl.size, int(mode), threshold is not None,
+                             0.0 if threshold is None else float(threshold), mask.ctypes.data,
+                             None if S is None else S.ctypes.data, None if sd is None else sd.ctypes.data,
+                             HOST_INPUTS | HOST_OUTPUTS, device, None))
+    return mask, sd

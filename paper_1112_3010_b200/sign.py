@@ -104,35 +104,29 @@ def classify(mu: ScalarField, mode: str, threshold: float | None = None) -> Scal
     """Interior mask: rint(mu) > 0 (2-D) / >= 1 (3-D) or mu >= threshold.
 
     Flagged nodes take the value of their nearest unflagged node (grid-index
-    metric, scipy's EDT tie-breaking) as R/sign.py:166-198 does.  This fill
-    runs on the host (SURVEY.md §8(f) rank 3 lists the GPU version as next).
+    metric) exactly as R/sign.py:166-198 does via scipy's EDT: the GPU runs the
+    same separable feature transform with the same tie rules
+    (csrc/classify.cu, checked against scipy in the tests).
     """
-    from scipy import ndimage
-
     if mode not in (WINDING_2D, DEGREE_3D):
         raise ValidationError(f"unknown classification mode {mode!r}")
-    vals = np.asarray(mu.values, dtype=np.float64).copy()
-    if mu.flagged_nodes is not None and mu.flagged_nodes.size:
-        fl = np.zeros(mu.grid.num_nodes, dtype=bool)
-        fl[mu.flagged_nodes] = True
-        if fl.all():
-            raise ValidationError("every node is flagged; cannot classify")
-        _, near = ndimage.distance_transform_edt(fl.reshape(mu.grid.shape), return_indices=True)
-        fill = vals.reshape(mu.grid.shape)[tuple(near)]
-        vals = np.where(fl, fill.reshape(-1), vals)
-    if threshold is not None:
-        inside = vals >= threshold
-    elif mode == WINDING_2D:
-        inside = np.rint(vals) > 0
-    else:
-        inside = np.rint(vals) >= 1
-    return ScalarField(mu.grid, inside.astype(np.float64), flagged_nodes=mu.flagged_nodes)
+    flagged = mu.flagged_nodes
+    if flagged is not None and flagged.size and np.unique(flagged).size >= mu.grid.num_nodes:
+        raise ValidationError("every node is flagged; cannot classify")
+    mask, _ = _native.classify(mu.grid.counts, mu.values, flagged if (flagged is not None and flagged.size) else None,
+                               1 if mode == WINDING_2D else 2, threshold)
+    return ScalarField(mu.grid, mask, flagged_nodes=mu.flagged_nodes)
 
 
 def signed_distance(s: ScalarField, mask: ScalarField) -> ScalarField:
+    """Positive inside, negative outside (R/sign.py:201-208)."""
     if mask.grid != s.grid:
         raise ValidationError("mask and distance field grids differ")
-    return ScalarField(s.grid, np.where(mask.values > 0.5, s.values, -s.values), s.flagged_nodes)
+    vals = np.asarray(s.values, dtype=np.float64)
+    m = np.asarray(mask.values, dtype=np.float64)
+    # `mask > 0.5` of the reference == `mask >= nextafter(0.5, 1)` (threshold rule)
+    _, sd = _native.classify(s.grid.counts, m, None, 1, float(np.nextafter(0.5, 1.0)), S=vals)
+    return ScalarField(s.grid, sd, s.flagged_nodes)
 
 
 _TWO_PI = 2.0 * math.pi

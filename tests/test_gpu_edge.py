@@ -142,3 +142,38 @@ def test_tau_sweep_matches_single_tau_runs(cuda_ok):
         ref = orc.run_config_unchecked(nodes, grid.counts, 1.0, tau)
         keep = ref["phi"] >= 1e-5 * ref["phi"].max()
         assert (np.abs(S - ref["S"])[keep] / np.maximum(np.abs(ref["S"][keep]), 1.0)).max() <= 1e-9
+
+
+@pytest.mark.parametrize("counts", [(40, 33), (17, 16, 15), (64,)])
+def test_gpu_classify_matches_scipy_fill(cuda_ok, counts):
+    """GPU nearest-unflagged fill + rounding == reference classify (scipy EDT), bit for bit."""
+    from paper_1112_3010_b200 import ScalarField, sign
+
+    grid = _grid(counts)
+    rng = rng_for(len(counts) * 7)
+    mu = rng.uniform(-0.6, 1.6, grid.num_nodes)
+    mode = "winding2d" if len(counts) != 3 else "degree3d"
+    for frac in (0.02, 0.3, 0.7):
+        flagged = np.sort(rng.choice(grid.num_nodes, int(frac * grid.num_nodes), replace=False))
+        field = ScalarField(grid, mu, flagged)
+        got = sign.classify(field, mode).values
+        ref = orc.classify(mu, flagged, counts, mode)
+        assert np.array_equal(got, ref)
+        got_t = sign.classify(field, mode, threshold=0.4).values
+        assert np.array_equal(got_t, orc.classify(mu, flagged, counts, mode, threshold=0.4))
+    S = rng.standard_normal(grid.num_nodes)
+    sd = sign.signed_distance(ScalarField(grid, S), ScalarField(grid, got)).values
+    assert np.array_equal(sd, np.where(got > 0.5, S, -S))
+
+
+def test_gpu_classify_c2_full_size(cuda_ok):
+    """C2: winding field + classify on the GPU vs the oracle's scipy fill on the same mu."""
+    from paper_1112_3010_b200 import PrecisionConfig, sign, workloads
+
+    d = workloads.c2()
+    mu = sign.winding_field(d["curve"], d["grid"], PrecisionConfig.native64(0.5))
+    got = sign.classify(mu, sign.WINDING_2D).values
+    ref = orc.classify(mu.values, mu.flagged_nodes, d["grid"].counts, "winding2d")
+    assert np.array_equal(got, ref)
+    inside = got.mean()
+    assert 0.2 < inside < 0.4  # star of radius ~600 in a 2048^2 grid
