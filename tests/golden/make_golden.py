@@ -53,7 +53,22 @@ def _subsample(n, count, seed):
     return np.sort(rng.choice(n, size=min(count, n), replace=False))
 
 
+def make_fieldio():
+    """EIKFLD01 bytes written by the reference writer (R/fieldio.py:31-64)."""
+    _import_reference()
+    from eikfld import fieldio, grid as grd, precision as prec
+
+    g = grd.GridSpec(origin=(-0.5, 0.25, 1.0), spacing=0.125, counts=(4, 5, 6))
+    vals = np.random.Generator(np.random.PCG64(8)).standard_normal(g.num_nodes)
+    f = grd.ScalarField(g, vals, flagged_nodes=[3, 77])
+    fieldio.write_field(os.path.join(HERE, "ref_field.fld"), f, "S", prec.PrecisionConfig.native64(0.1),
+                        {"method": "fft", "k": 1})
+    print("wrote ref_field.fld")
+
+
 def main():
+    if "--only-fieldio" in sys.argv:
+        return make_fieldio()
     conv, der, dist, grd, prec, sgn = _import_reference()
     sys.path.insert(0, REPO)
     from paper_1112_3010_b200 import workloads as wl
