@@ -65,6 +65,12 @@ struct RowCfg {
   static constexpr int NBUF = (LH <= 10 && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
   using XB = XBuf<NBUF>;
   static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
+  // resident CTAs per SM requested from the register allocator (128 threads:
+  // 4 CTAs = 16 warps at <= 128 registers)
+#ifndef EIK_ROW_MINB128
+#define EIK_ROW_MINB128 4
+#endif
+  static constexpr int MINB = (NT <= 128 && LN::EPT <= 8) ? EIK_ROW_MINB128 : (NT <= 256 ? 2 : 1);
 };
 
 // Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
@@ -654,7 +660,7 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
 }
 
 template <int LH>
-__global__ void __launch_bounds__(RowCfg<LH>::NT, (RowCfg<LH>::NT <= 256) ? 2 : 1) row_kernel(const __grid_constant__ RowArgs a) {
+__global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(const __grid_constant__ RowArgs a) {
   using LN = typename RowCfg<LH>::LN;
   constexpr int LPC = RowCfg<LH>::LPC;
   constexpr int E = LN::EPT;
