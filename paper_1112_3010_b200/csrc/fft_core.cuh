@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tmem.cuh"
+
 namespace eik {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -244,6 +246,7 @@ struct TwSrc {
   const double2* st;
   const double2* q;
   int lq;
+  uint32_t tm;  // TMEM address of this thread's cached radix-16 quarter-stage twiddles (0 = none)
 };
 
 template <class LN, bool INV, int S>
@@ -291,10 +294,34 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
     const int b = t + g * LN::TPL;
     if constexpr (NS > 1) {
       const int k = b & (NS - 1);
+      bool done = false;
+      if constexpr (LN::st_quarter(INV, S) && G == 1 && R == 16) {
+        if (tw.tm) {  // per-thread constants cached in TMEM: 4 x (16-word load, wait), no table math
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const double2 w = st_tw<LN, INV, S>(tw, k, r);
-        v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
+          for (int c = 0; c < 4; ++c) {
+            uint32_t w32[16];
+            tmem_ld16(tw.tm + 16 * c, w32);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int r = 4 * c + q;  // TMEM holds W^{k r} at complex slot r (slot 0 unused)
+              if (r >= 1) {
+                const double2 w = make_double2(
+                    __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 1] << 32) | w32[4 * q])),
+                    __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 3] << 32) | w32[4 * q + 2])));
+                v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+              }
+            }
+          }
+          done = true;
+        }
+      }
+      if (!done) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const double2 w = st_tw<LN, INV, S>(tw, k, r);
+          v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
+        }
       }
     }
     dft<R, INV, HALF_IN && S == 0>(&v[g * R]);

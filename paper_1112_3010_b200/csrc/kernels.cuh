@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
-  const TwSrc tws{sts, twq, L};
+  const TwSrc tws{sts, twq, L, 0u};
 
   double2 v[LN::EPT];
   if constexpr (OUT == OUT_COMPS) {
@@ -304,8 +304,12 @@ struct TmCfg {
   using LN = Line<L, 16>;
   static constexpr int NT = LN::TPL > 256 ? LN::TPL : 256;
   static constexpr int LPC = NT / LN::TPL;
-  static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread
-  static constexpr int NEED = (NT / 128) * WPT;
+  static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
+  // 4096-point lines: the radix-16 NS=256 stage's twiddles W^{t r} are per-thread
+  // constants shared by the forward and every inverse -> cached in TMEM too
+  static constexpr bool TWC = (L == 12) && LN::INV_SHARES;
+  static constexpr int WPT_ALL = WPT + (TWC ? 64 : 0);
+  static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
 };
@@ -328,8 +332,17 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
   const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle tables
-  const TwSrc tws{sts, twq, L};
-  const uint32_t ta = tmem_thread_addr(tbase, TC::WPT);
+  const uint32_t ta = tmem_thread_addr(tbase, TC::WPT_ALL);
+  uint32_t ttw = 0;
+  if constexpr (TC::TWC) {
+    ttw = ta + TC::WPT;
+    double2 w[16];
+    w[0] = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) w[r] = twq_get(twq, L, t * r);  // W_4096^{t r}, k = t at NS = 256
+    tmem_put(ttw, w);
+  }
+  const TwSrc tws{sts, twq, L, ttw};
 
   double2 v[LN::EPT];
   if constexpr (OUT == OUT_SUM) {
@@ -430,7 +443,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
-  const TwSrc tws{sts, twq, L};
+  const TwSrc tws{sts, twq, L, 0u};
   const int64_t o = valid ? l / a.inner : 0, q = valid ? l % a.inner : 0;
   const double2* src = a.in[c] + o * a.outer_in + q;
   double2* dst = a.out[c] + o * a.outer_out + q;
@@ -583,7 +596,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
   twq_fill(twq, LQ, tw, lmax);
   st_fill<LN>(sts, tw, lmax);
   __syncthreads();
-  const TwSrc tws{sts, twq, LQ};
+  const TwSrc tws{sts, twq, LQ, 0u};
   double2 v[LN::EPT];
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
@@ -656,7 +669,7 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
       z[r] = make_double2(0.0, 0.0);
     }
   }
-  fft_line<LN, true>(z, t, xb, TwSrc{sts, twq, LN::L + 1});
+  fft_line<LN, true>(z, t, xb, TwSrc{sts, twq, LN::L + 1, 0u});
 }
 
 template <int LH>
