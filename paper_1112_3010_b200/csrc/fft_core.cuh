@@ -129,8 +129,6 @@ __device__ __forceinline__ void dft(double2* a) {
   }
 }
 
-__device__ __forceinline__ int spad(int i) { return i + (i >> 3); }
-
 // Quarter-wave twiddle table in shared memory: q[k] = W_Q^k = exp(-2 pi i k / Q),
 // k in [0, Q/4), Q = 2^lq.  Any W_Q^j is one table read plus a quadrant rotation,
 // so the table for a 4096-point line is ~19 KB instead of 64 KB.  Stage
@@ -156,7 +154,12 @@ __device__ __forceinline__ void twq_fill(double2* q, int lq, const double2* __re
 
 // Compile-time description of a length-2^L line transform with at most E
 // elements (and radix) per thread.
-template <int L_, int E_ = 16>
+// Exchange-buffer padding: element i of a line lives at slot
+// i + (i >> PA) + (i >> PB) (PB = 0: no second term) and consecutive lines of a
+// CTA are SMEM = pad(M-1) + 1 + XT slots apart.  The defaults suit line-major
+// lines; the kernel configurations pick (PA, PB, XT) per shape so that every
+// exchange store and load is free of bank conflicts (tools/bank_sim.py).
+template <int L_, int E_ = 16, int PA = 3, int PB = 0, int XT = 2>
 struct Line {
   static constexpr int L = L_;
   static constexpr int E = E_;
@@ -167,7 +170,8 @@ struct Line {
   static constexpr int NST = (L == 0) ? 0 : ((L <= LE) ? 1 : (L + LE - 1) / LE);
   static constexpr int R0 = (L <= LE) ? M : ((L % LE) ? (1 << (L % LE)) : E);
   static constexpr int RL = (NST <= 1) ? R0 : E;
-  static constexpr int SMEM = M + (M >> 3) + 1;  // padded double2 slots per line
+  __host__ __device__ static constexpr int pad(int i) { return i + (i >> PA) + (PB ? (i >> PB) : 0); }
+  static constexpr int SMEM = pad(M - 1) + 1 + XT;  // padded double2 slots per line
   static constexpr int TWQ = tpos_size((L >= 2) ? (M >> 2) : 1);  // quarter-table slots (own resolution)
   __host__ __device__ static constexpr int frad(int s) { return s == 0 ? R0 : E; }
   __host__ __device__ static constexpr int rad(bool inv, int s) { return inv ? frad(NST - 1 - s) : frad(s); }
@@ -333,7 +337,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
       const int b = t + g * LN::TPL;
       const int o = (b / NS) * NS * R + (b & (NS - 1));
 #pragma unroll
-      for (int r = 0; r < R; ++r) sm[spad(o + r * NS)] = v[g * R + r];
+      for (int r = 0; r < R; ++r) sm[LN::pad(o + r * NS)] = v[g * R + r];
     }
     __syncthreads();
     constexpr int R2 = LN::rad(INV, S + 1);
@@ -342,7 +346,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
     for (int g = 0; g < G2; ++g) {
       const int b = t + g * LN::TPL;
 #pragma unroll
-      for (int r = 0; r < R2; ++r) v[g * R2 + r] = sm[spad(b + r * (LN::M / R2))];
+      for (int r = 0; r < R2; ++r) v[g * R2 + r] = sm[LN::pad(b + r * (LN::M / R2))];
     }
     xb.done();
   }

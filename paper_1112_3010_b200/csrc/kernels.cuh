@@ -42,9 +42,31 @@ enum { SPEC_COMPLEX = 0, SPEC_REAL_T = 1, SPEC_IMAG_T = 2, SPEC_COMPLEX_T = 3 };
 #endif
 __host__ __device__ constexpr int col_e(int L) { return (L >= 10 && L <= 12) ? EIK_COL_E_LARGE : 16; }
 __host__ __device__ constexpr int col_threads(int L) { return L >= 10 ? 512 : 256; }
+// Exchange-buffer padding per launch shape, packed as PA | PB << 4 | XT << 8
+// (see Line): the bank-conflict-free choices of tools/bank_sim.py for the
+// column mapping (line = tid % LPC: col, lines and TMEM kernels) and the row
+// mapping (line = tid / TPL).  Shapes not listed are conflict-free already.
+__host__ __device__ constexpr int pad_code(int pa, int pb, int xt) { return pa | (pb << 4) | (xt << 8); }
+constexpr int PAD_DEFAULT = 3 | (0 << 4) | (2 << 8);
+__host__ __device__ constexpr int col_pad(int L) {
+  return (col_e(L) == 8 && L == 10) ? pad_code(3, 0, 3)
+       : (col_e(L) == 8 && L == 11) ? pad_code(2, 4, 6)
+       : (L == 13) ? pad_code(3, 4, 0) : PAD_DEFAULT;
+}
+__host__ __device__ constexpr int tm_pad(int L) {
+  return L == 10 ? pad_code(2, 4, 0) : L == 11 ? pad_code(3, 5, 6) : L == 12 ? pad_code(4, 0, 0)
+       : L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT;
+}
+__host__ __device__ constexpr int row_pad(int LH) {
+  return LH == 5 ? pad_code(4, 0, 1) : LH == 6 ? pad_code(2, 4, 2) : LH == 7 ? pad_code(3, 6, 0)
+       : LH == 8 ? pad_code(4, 0, 0) : PAD_DEFAULT;
+}
+template <int L, int E, int CODE>
+using PaddedLine = Line<L, E, (CODE & 15), ((CODE >> 4) & 15), (CODE >> 8)>;
+
 template <int L>
 struct ColCfg {
-  using LN = Line<L, col_e(L)>;
+  using LN = PaddedLine<L, col_e(L), col_pad(L)>;
   static constexpr int NT = (col_threads(L) > LN::TPL) ? col_threads(L) : LN::TPL;
   static constexpr int LPC = NT / LN::TPL;
   // ping-pong exchange buffers (one barrier per exchange instead of two) where
@@ -58,7 +80,7 @@ struct ColCfg {
 __host__ __device__ constexpr int row_e(int LH) { return LH >= 9 ? 8 : 16; }
 template <int LH>
 struct RowCfg {
-  using LN = Line<LH, row_e(LH)>;
+  using LN = PaddedLine<LH, row_e(LH), row_pad(LH)>;
   static constexpr int NT = (LN::TPL >= 128) ? LN::TPL : 128;
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
@@ -301,7 +323,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 // results); E = 16, 256+ threads, two CTAs per SM.
 template <int L>
 struct TmCfg {
-  using LN = Line<L, 16>;
+  using LN = PaddedLine<L, 16, tm_pad(L)>;
   static constexpr int NT = LN::TPL > 256 ? LN::TPL : 256;
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
@@ -608,12 +630,12 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
   // did not use), then split into X[k], k in [0, MH]
   double2* sm = xb.cur();
 #pragma unroll
-  for (int r = 0; r < LN::EPT; ++r) sm[spad(LN::out_idx(t, r))] = v[r];
+  for (int r = 0; r < LN::EPT; ++r) sm[LN::pad(LN::out_idx(t, r))] = v[r];
   __syncthreads();
   if (!valid) return;
   for (int k = t; k <= MH; k += LN::TPL) {
-    const double2 zk = sm[spad(k & (MH - 1))];
-    const double2 zc = sm[spad((MH - k) & (MH - 1))];
+    const double2 zk = sm[LN::pad(k & (MH - 1))];
+    const double2 zc = sm[LN::pad((MH - k) & (MH - 1))];
     const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y - zc.y));   // (Z[k] + conj Z[-k]) / 2
     const double2 d = make_double2(0.5 * (zk.y + zc.y), -0.5 * (zk.x - zc.x));  // (Z[k] - conj Z[-k]) / (2i)
     const double2 w = twq_get(twq, LQ, k);                                     // W_M^k (k = MH -> -1)
