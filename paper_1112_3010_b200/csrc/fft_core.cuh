@@ -161,6 +161,7 @@ __device__ __forceinline__ void twq_fill(double2* q, int lq, const double2* __re
 // exchange store and load is free of bank conflicts (tools/bank_sim.py).
 template <int L_, int E_ = 16, int PA = 3, int PB = 0, int XT = 2>
 struct Line {
+  static constexpr bool FOUR_STEP = false;
   static constexpr int L = L_;
   static constexpr int E = E_;
   static constexpr int LE = ilog2c(E_);
@@ -241,8 +242,15 @@ __device__ __forceinline__ void st_fill_stage(double2* sts, const double2* __res
 }
 template <class LN>
 __device__ __forceinline__ void st_fill(double2* sts, const double2* __restrict__ gtw, int lmax) {
-  st_fill_stage<LN, false, 0>(sts, gtw, lmax);
-  st_fill_stage<LN, true, 0>(sts, gtw, lmax);
+  if constexpr (LN::FOUR_STEP) {
+    for (int i = threadIdx.x; i < LN::ST_SIZE; i += blockDim.x) {  // W_256^{j a}, row j, column a-1
+      const int j = i / 15, a = i % 15 + 1;
+      sts[i] = __ldg(gtw + ((int64_t)(j * a) << (lmax - 8)));
+    }
+  } else {
+    st_fill_stage<LN, false, 0>(sts, gtw, lmax);
+    st_fill_stage<LN, true, 0>(sts, gtw, lmax);
+  }
 }
 
 // Twiddle sources of a line: stage tables + the quarter-wave table (resolution 2^lq >= M).
@@ -360,12 +368,130 @@ __device__ __forceinline__ void stages_from(double2 (&v)[LN::EPT], int t, XB& xb
   }
 }
 
+// ---------------------------------------------------------------------------
+// 4096-point lines as 16 x 256 ("four-step"), 256 threads per line.
+//
+// The Stockham schedule exchanges the whole line through shared memory twice
+// per transform, each time with CTA-wide barriers, so the 8 warps of a CTA
+// move in lock-step between the FP64 and the shared-memory phases.  Here
+// n = n2 + 256 n1 and k = k1 + 16 k2: a 16-point DFT over n1 in registers
+// (thread t = n2), the twiddle W_4096^{n2 k1} (per-thread constants), ONE
+// CTA-wide exchange that hands row k1 to half-warp k1, then the 256-point DFT
+// of that row inside its half-warp (16 x 16, exchange through the row's own
+// buffer with __syncwarp only).  Forward output / inverse input layout:
+//   register i of thread t holds k = (t >> 4) + 16 (t & 15) + 256 i
+// Forward input / inverse output: n = t + 256 i (as the Stockham layout).
+// Exchange buffer: 16 rows of PITCH slots; the in-row 16 x 16 transpose uses
+// a stride of 17 so both sides are free of bank conflicts.
+struct Line4K {
+  static constexpr bool FOUR_STEP = true;
+  static constexpr int L = 12, E = 16, M = 4096, EPT = 16, TPL = 256, R0 = 16, RL = 16, NST = 3;
+  static constexpr int PITCH = 272;
+  static constexpr int SMEM = 16 * PITCH;
+  static constexpr int TWQ = tpos_size(M >> 2);
+  static constexpr bool INV_SHARES = true;
+  static constexpr int ST_SIZE = 16 * 15;  // W_256^{j a}, j < 16, 1 <= a < 16
+  __device__ static __forceinline__ int in_idx(int t, int i) { return t + 256 * i; }
+  __device__ static __forceinline__ int out_idx(int t, int i) { return (t >> 4) + 16 * (t & 15) + 256 * i; }
+  __device__ static __forceinline__ constexpr bool upper_in(int i) { return i >= 8; }
+};
+
+// v[r] *= W_4096^{t r} (or its conjugate), r = 1..15: TMEM cache or quarter table
+template <bool INV>
+__device__ __forceinline__ void f4k_twiddle_t(double2 (&v)[16], int t, const TwSrc& tw) {
+  if (tw.tm) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t w32[16];
+      tmem_ld16(tw.tm + 16 * c, w32);
+      tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = 4 * c + q;
+        if (r >= 1) {
+          const double2 w = make_double2(
+              __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 1] << 32) | w32[4 * q])),
+              __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 3] << 32) | w32[4 * q + 2])));
+          v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      const double2 w = twq_get(tw.q, tw.lq, (t * r) << (tw.lq - 12));
+      v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+    }
+  }
+}
+
+// v[r] *= W_256^{x r} (or conjugate), x = t & 15, from the stage table
+template <bool INV>
+__device__ __forceinline__ void f4k_twiddle_row(double2 (&v)[16], int x, const TwSrc& tw) {
+  const double2* row = tw.st + x * 15 - 1;
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = INV ? cmulc(v[r], row[r]) : cmul(v[r], row[r]);
+}
+
+template <bool HALF_IN>
+__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, double2* sm, const TwSrc& tw) {
+  constexpr int P = Line4K::PITCH;
+  const int g = t >> 4, x = t & 15;
+  double2* row = sm + g * P;
+  dft<16, false, HALF_IN>(v);  // over n1: v[k1], thread t = n2
+  f4k_twiddle_t<false>(v, t, tw);
+  __syncthreads();  // every thread is done with the buffer (previous transform)
+#pragma unroll
+  for (int r = 0; r < 16; ++r) sm[r * P + t] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = row[x + 16 * m];  // row k1 = g, n2 = x + 16 m
+  dft<16, false, false>(v);                             // over m: v[a], lane x = j
+  f4k_twiddle_row<false>(v, x, tw);
+  __syncwarp();
+#pragma unroll
+  for (int a = 0; a < 16; ++a) row[a * 17 + x] = v[a];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = row[x * 17 + j];  // lane x = a
+  dft<16, false, false>(v);                             // over j: v[b] = X[g + 16 x + 256 b]
+}
+
+__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, double2* sm, const TwSrc& tw) {
+  constexpr int P = Line4K::PITCH;
+  const int g = t >> 4, x = t & 15;
+  double2* row = sm + g * P;
+  dft<16, true, false>(v);  // over b: v[j], lane x = a
+  f4k_twiddle_row<true>(v, x, tw);
+  __syncwarp();  // the row is only touched by this half-warp since the last CTA barrier
+#pragma unroll
+  for (int j = 0; j < 16; ++j) row[x * 17 + j] = v[j];
+  __syncwarp();
+#pragma unroll
+  for (int a = 0; a < 16; ++a) v[a] = row[a * 17 + x];  // lane x = j
+  dft<16, true, false>(v);                              // over a: v[m] = z[x + 16 m]
+  __syncwarp();
+#pragma unroll
+  for (int m = 0; m < 16; ++m) row[x + 16 * m] = v[m];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = sm[r * P + t];  // thread t = n2: v[k1]
+  __syncthreads();  // buffer free again: the next transform may write any row
+  f4k_twiddle_t<true>(v, t, tw);
+  dft<16, true, false>(v);  // over k1: v[i] = x[t + 256 i]
+}
+
 // Full transform of the line held in v (layouts documented above).
 // HALF_IN (forward only): input elements >= M/2 are zero and their registers are not read.
 template <class LN, bool INV, bool HALF_IN = false, class XB>
 __device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw) {
   static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
-  stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, tw);
+  if constexpr (LN::FOUR_STEP) {
+    if constexpr (INV) f4k_inverse(v, t, xb.b0, tw);
+    else f4k_forward<HALF_IN>(v, t, xb.b0, tw);
+  } else {
+    stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, tw);
+  }
 }
 
 }  // namespace eik

@@ -24,6 +24,8 @@
 #include "fft_core.cuh"
 #include "tmem.cuh"
 
+#include <type_traits>
+
 namespace eik {
 
 constexpr int MAXC = 8;
@@ -321,9 +323,12 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 // Column pass, distance group, with the forward spectrum parked in TMEM.
 // Same arithmetic as col_kernel<L, IN, OUT_COMPS, HALF> (bit-identical
 // results); E = 16, 256+ threads, two CTAs per SM.
+#ifndef EIK_FOUR_STEP
+#define EIK_FOUR_STEP 1
+#endif
 template <int L>
 struct TmCfg {
-  using LN = PaddedLine<L, 16, tm_pad(L)>;
+  using LN = std::conditional_t<(L == 12 && EIK_FOUR_STEP), Line4K, PaddedLine<L, 16, tm_pad(L)>>;
   static constexpr int NT = LN::TPL > 256 ? LN::TPL : 256;
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
