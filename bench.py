@@ -336,6 +336,14 @@ def main():
     pts_per_step_job = B * N * world
     value = pts_per_step_job * a.steps / (total_ms / 1e3)
 
+    # ---- phi validity band (untimed): fraction of nodes with phi >= 1e-5 / 1e-9 / 1e-13
+    # (throughput counts every node, the valid band is reported beside it)
+    phi_d = torch.empty(B * N, dtype=torch.float64, device=dev)
+    plan.run(nodes_d, offs_d, B, None, None, phi=phi_d, host=False, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    validity = {f"phi>={t:g}": round(float((phi_d >= t).double().mean().item()), 6) for t in (1e-5, 1e-9, 1e-13)}
+    del phi_d
+
     # ---- end to end through the C-ABI with pinned HOST buffers
     def pinned(n, dtype):
         return torch.empty(n, dtype=dtype, pin_memory=True).numpy()
@@ -410,6 +418,7 @@ def main():
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic, "kernel": dom, "algorithmic_bytes": alg[dom],
                 "kernel_ms": round(mean_pass[dom], 5), "peak_source": peak_src,
+                "peak_nominal": 8000.0, "frac_nominal": round(ach / 8000.0, 4),
                 "step_bytes": sum(alg.values()),
                 "step_frac": round(sum(alg.values()) / (total_ms / a.steps / 1e3) / 1e9 / peak, 4)}
 
@@ -440,6 +449,7 @@ def main():
                     "d2h_bytes_per_step": int(d2h), "steps": ke},
             "gpu_launches": launches_per_step * a.steps,
             "pass_ms": {k: round(v, 5) for k, v in mean_pass.items()},
+            "phi_validity": validity,
             "roofline": roof,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
