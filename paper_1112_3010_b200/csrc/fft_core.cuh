@@ -278,18 +278,29 @@ __device__ __forceinline__ double2 st_tw(const TwSrc& tw, int k, int r) {
 }
 
 // Exchange buffers of one line.  With NBUF = 2 consecutive exchanges alternate
-// between two buffers, so a stage needs one __syncthreads (between its writes
-// and its reads) instead of two: writes of exchange k+2 cannot overtake reads
-// of exchange k because every thread passed the barrier of exchange k+1.
-template <int NBUF>
+// between two buffers, so a stage needs one barrier (between its writes and
+// its reads) instead of two: writes of exchange k+2 cannot overtake reads of
+// exchange k because every thread passed the barrier of exchange k+1.
+// SYNC selects the barrier that covers exactly the threads of one line:
+// 0 = the CTA (__syncthreads), 1 = the warp (lines of <= 32 threads, whole
+// lines per warp), 2 = named barrier `bar` over the NTH threads of the line
+// (line-major CTAs holding several lines), so lines of a CTA do not wait on
+// each other.
+template <int NBUF, int SYNC = 0, int NTH = 0>
 struct XBuf {
   double2* b0;
   double2* b1;
   int ph;
+  int bar;
   __device__ __forceinline__ double2* cur() const { return (NBUF == 2 && ph) ? b1 : b0; }
+  __device__ __forceinline__ void sync() const {
+    if constexpr (SYNC == 1) __syncwarp();
+    else if constexpr (SYNC == 2) asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "n"(NTH) : "memory");
+    else __syncthreads();
+  }
   __device__ __forceinline__ void done() {
     if constexpr (NBUF == 2) ph ^= 1;
-    else __syncthreads();
+    else sync();
   }
 };
 
@@ -347,7 +358,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
 #pragma unroll
       for (int r = 0; r < R; ++r) sm[LN::pad(o + r * NS)] = v[g * R + r];
     }
-    __syncthreads();
+    xb.sync();
     constexpr int R2 = LN::rad(INV, S + 1);
     constexpr int G2 = LN::EPT / R2;
 #pragma unroll
