@@ -50,14 +50,18 @@ __host__ __device__ constexpr int col_threads(int L) { return L >= 10 ? 512 : 25
 // mapping (line = tid / TPL).  Shapes not listed are conflict-free already.
 __host__ __device__ constexpr int pad_code(int pa, int pb, int xt) { return pa | (pb << 4) | (xt << 8); }
 constexpr int PAD_DEFAULT = 3 | (0 << 4) | (2 << 8);
-// Column-type kernels interleave the lines of a CTA across the threads
-// (line = tid % LPC) so that every warp load/store covers LPC adjacent columns
-// (full 32-byte sectors).  EIK_LINE_MAJOR=1 maps them line-major instead, which
-// lets each line synchronise with its own barrier, but was measured slower
-// (C3 column pass 1.9 -> 3.5 ms): the sector efficiency matters more.
-#ifndef EIK_LINE_MAJOR
-#define EIK_LINE_MAJOR 0
+// Column-type kernels interleave the LPC lines of a CTA across its threads
+// (line = tid % LPC under __syncthreads), so one warp load/store covers LPC
+// adjacent columns of only 32/LPC rows: few 128-byte lines per request.
+// EIK_COL_IL = IL < LPC interleaves groups of IL lines over IL*TPL threads,
+// each group with its own (warp / named) barrier.  Measured slower: C3 column
+// pass 1.88 ms (IL = LPC) vs 2.51 (IL = 2) vs 3.52 (IL = 1, line-major),
+// C5 6.98 vs 7.33 vs 7.78 ms; the cache lines touched per warp request cost
+// more than the narrower barriers save.
+#ifndef EIK_COL_IL
+#define EIK_COL_IL 0
 #endif
+__host__ __device__ constexpr int col_il(int lpc) { return (EIK_COL_IL == 0 || EIK_COL_IL >= lpc) ? lpc : EIK_COL_IL; }
 __host__ __device__ constexpr int tpl_of(int L, int E) { return (1 << L) <= E ? 1 : (1 << L) / E; }
 // line-major (row) mapping, E = 16 lines, by L (tools/bank_sim.py, mapping "row")
 __host__ __device__ constexpr int lm_pad16(int L) {
@@ -65,13 +69,19 @@ __host__ __device__ constexpr int lm_pad16(int L) {
        : L == 8 ? pad_code(4, 0, 0) : L == 9 ? pad_code(3, 4, 0) : L == 10 ? pad_code(4, 0, 0)
        : L == 11 ? pad_code(3, 6, 0) : L == 12 ? pad_code(4, 0, 0) : L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT;
 }
-__host__ __device__ constexpr int col_pad(int L, bool lm) {
-  return col_e(L) == 16 ? (lm ? lm_pad16(L) : (L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT))
-       : lm ? PAD_DEFAULT
+// pair-interleaved (IL = 2 < LPC) pads
+__host__ __device__ constexpr int il2_pad(int L, int E) {
+  return E == 8 ? (L == 10 ? pad_code(2, 3, 6) : PAD_DEFAULT)
+       : L == 7 ? pad_code(3, 5, 2) : L == 8 ? pad_code(4, 0, 5) : (L == 9 || L == 10) ? pad_code(2, 4, 6)
+       : PAD_DEFAULT;
+}
+__host__ __device__ constexpr int col_pad(int L, bool pair) {
+  return pair ? il2_pad(L, col_e(L))
+       : col_e(L) == 16 ? (L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT)
        : (L == 10) ? pad_code(3, 0, 3) : (L == 11) ? pad_code(2, 4, 6) : PAD_DEFAULT;
 }
-__host__ __device__ constexpr int tm_pad(int L, bool lm) {
-  return lm ? lm_pad16(L)
+__host__ __device__ constexpr int tm_pad(int L, bool pair) {
+  return pair ? il2_pad(L, 16)
        : L == 10 ? pad_code(2, 4, 0) : L == 11 ? pad_code(3, 5, 6) : L == 12 ? pad_code(4, 0, 0)
        : L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT;
 }
@@ -79,9 +89,9 @@ __host__ __device__ constexpr int row_pad(int LH) {
   return LH == 5 ? pad_code(4, 0, 1) : LH == 6 ? pad_code(2, 4, 2) : LH == 7 ? pad_code(3, 6, 0)
        : LH == 8 ? pad_code(4, 0, 0) : PAD_DEFAULT;
 }
-// barrier covering one line (see XBuf)
-__host__ __device__ constexpr int line_sync(bool lm, int lpc, int tpl) {
-  return lpc == 1 ? 0 : !lm ? 0 : tpl <= 32 ? 1 : 2;
+// barrier covering one group of il interleaved lines (see XBuf)
+__host__ __device__ constexpr int group_sync(int il, int lpc, int tpl) {
+  return il >= lpc ? 0 : il * tpl <= 32 ? 1 : 2;
 }
 template <int L, int E, int CODE>
 using PaddedLine = Line<L, E, (CODE & 15), ((CODE >> 4) & 15), (CODE >> 8)>;
@@ -91,14 +101,14 @@ struct ColCfg {
   static constexpr int TPL0 = tpl_of(L, col_e(L));
   static constexpr int NT = (col_threads(L) > TPL0) ? col_threads(L) : TPL0;
   static constexpr int LPC = NT / TPL0;
-  static constexpr bool LM = EIK_LINE_MAJOR && LPC > 1;
-  using LN = PaddedLine<L, col_e(L), col_pad(L, LM)>;
-  __device__ static __forceinline__ int line_of(int tid) { return LM ? tid / TPL0 : tid % LPC; }
-  __device__ static __forceinline__ int t_of(int tid) { return LM ? tid % TPL0 : tid / LPC; }
+  static constexpr int IL = col_il(LPC);
+  using LN = PaddedLine<L, col_e(L), col_pad(L, IL == 2 && LPC > 2)>;
+  __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
+  __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
   // ping-pong exchange buffers (one barrier per exchange instead of two) where
   // they were measured to pay off without costing occupancy (C5-sized lines)
   static constexpr int NBUF = ((L == 10 || L == 11) && (2 * LPC * LN::SMEM + LN::TWQ) * 16 <= 200 * 1024) ? 2 : 1;
-  using XB = XBuf<NBUF, line_sync(LM, LPC, TPL0), TPL0>;
+  using XB = XBuf<NBUF, group_sync(IL, LPC, TPL0), IL * TPL0>;
   static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
 };
 // Row kernels (c2r / r2c along the contiguous last axis): complex lines of
@@ -111,7 +121,7 @@ struct RowCfg {
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
   static constexpr int NBUF = (LH <= 10 && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
-  using XB = XBuf<NBUF, line_sync(true, LPC, LN::TPL), LN::TPL>;  // row kernels are line-major
+  using XB = XBuf<NBUF, group_sync(1, LPC, LN::TPL), LN::TPL>;  // row kernels are line-major
   static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
   // resident CTAs per SM requested from the register allocator (128 threads:
   // 4 CTAs = 16 warps at <= 128 registers)
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   const bool valid = l < a.nlines;
   const int64_t item = blockIdx.y;
   using CC = ColCfg<L>;
-  typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line};
+  typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line / CC::IL};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
@@ -355,11 +365,11 @@ struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
   static constexpr int NT = TPL0 > 256 ? TPL0 : 256;
   static constexpr int LPC = NT / TPL0;
-  static constexpr bool LM = EIK_LINE_MAJOR && LPC > 1;
-  using LN = std::conditional_t<(L == 12 && EIK_FOUR_STEP), Line4K, PaddedLine<L, 16, tm_pad(L, LM)>>;
-  using XB = XBuf<1, line_sync(LM, LPC, TPL0), TPL0>;
-  __device__ static __forceinline__ int line_of(int tid) { return LM ? tid / TPL0 : tid % LPC; }
-  __device__ static __forceinline__ int t_of(int tid) { return LM ? tid % TPL0 : tid / LPC; }
+  static constexpr int IL = col_il(LPC);
+  using LN = std::conditional_t<(L == 12 && EIK_FOUR_STEP), Line4K, PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>;
+  using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
+  __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
+  __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
   // 4096-point lines: the radix-16 NS=256 stage's twiddles W^{t r} are per-thread
   // constants shared by the forward and every inverse -> cached in TMEM too
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
   const int64_t l = (int64_t)blockIdx.x * LPC + line;
   const bool valid = l < a.nlines;
   const int64_t item = blockIdx.y;
-  typename TC::XB xb{smem + line * LN::SMEM, nullptr, 0, 1 + line};
+  typename TC::XB xb{smem + line * LN::SMEM, nullptr, 0, 1 + line / TC::IL};
   double2* twq = smem + LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
   uint32_t* slot = reinterpret_cast<uint32_t*>(sts + LN::ST_SIZE);
@@ -493,7 +503,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   const bool valid = l < a.nlines;
   const int c = blockIdx.y;
   using CC = ColCfg<L>;
-  typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line};
+  typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line / CC::IL};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);

@@ -48,7 +48,7 @@ def exchanges(L, E, inv):
     return [ins for ex in out for ins in ex]
 
 
-def cost(L, E, LPC, addr, mapping="col"):
+def cost(L, E, LPC, addr, mapping="col", il=None):
     M, EPT, TPL, NST, frad = line_params(L, E)
     NT = LPC * TPL
     total = ideal = 0
@@ -60,6 +60,9 @@ def cost(L, E, LPC, addr, mapping="col"):
                     for tid in range(w0 + 8 * p, w0 + 8 * p + 8):
                         if mapping == "col":
                             line, t = tid % LPC, tid // LPC
+                        elif mapping == "il":  # groups of il lines interleaved over il*TPL threads
+                            grp = il * TPL
+                            line, t = (tid // grp) * il + tid % il, (tid % grp) // il
                         else:
                             line, t = tid // TPL, tid % TPL
                         a = addr(line, ins[t])
