@@ -140,6 +140,12 @@ struct KSpec {
   int64_t ld;
   int imag;
   int odd0;
+  // Optional register-order copy (real/imaginary spectra, 2-D plans): the value
+  // register r of thread tid of CTA tile b needs, at perm[(b * EPT + r) * NT + tid],
+  // unfolded with the axis-0 parity sign applied.  Warp loads are contiguous
+  // (a column kernel otherwise touches one cache line per lane).  When set,
+  // odd0 is 0 (the sign is baked in).
+  const double* perm;
 };
 
 struct ColArgs {
@@ -188,6 +194,12 @@ __device__ __forceinline__ double2 kmul(double2 x, const KSpec& k, int64_t l, in
 __device__ __forceinline__ double kload(const KSpec& k, int64_t l, int k0, int M0) {
   const bool hi = k0 > (M0 >> 1);
   return __ldg(k.re + (int64_t)(hi ? M0 - k0 : k0) * k.ld + l);
+}
+// kload for a kernel of configuration CFG (register r of this thread)
+template <class CFG>
+__device__ __forceinline__ double kload_c(const KSpec& k, int64_t l, int k0, int M0, int r) {
+  if (k.perm) return __ldg(k.perm + ((int64_t)blockIdx.x * CFG::LN::EPT + r) * CFG::NT + threadIdx.x);
+  return kload(k, l, k0, M0);
 }
 __device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0) {
   if (k.odd0 && k0 > (M0 >> 1)) v = -v;
@@ -276,7 +288,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     double kn[LN::EPT];  // next component's kernel spectrum, prefetched
     if (real_ks && valid) {
 #pragma unroll
-      for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[0], l, LN::out_idx(t, r), LN::M);
+      for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<ColCfg<L>>(a.ks[0], l, LN::out_idx(t, r), LN::M, r);
     }
 #pragma unroll 1
     for (int j = 0; j < a.n_comp; ++j) {
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
         for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M) : v[r];
         if (j + 1 < a.n_comp && valid) {
 #pragma unroll
-          for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[j + 1], l, LN::out_idx(t, r), LN::M);
+          for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<ColCfg<L>>(a.ks[j + 1], l, LN::out_idx(t, r), LN::M, r);
         }
       } else {
 #pragma unroll
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       double kn[LN::EPT];  // this input's kernel spectrum, loaded before its transform
       if (real_ks && valid) {
 #pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[i], l, LN::out_idx(t, r), LN::M);
+        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<ColCfg<L>>(a.ks[i], l, LN::out_idx(t, r), LN::M, r);
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
       double kn[LN::EPT];
       if (valid) {
 #pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[i], l, LN::out_idx(t, r), LN::M);
+        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<TC>(a.ks[i], l, LN::out_idx(t, r), LN::M, r);
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
   double kn[LN::EPT];
   if (valid) {
 #pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[0], l, LN::out_idx(t, r), LN::M);
+    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<TC>(a.ks[0], l, LN::out_idx(t, r), LN::M, r);
   }
 #pragma unroll 1
   for (int j = 0; j < a.n_comp; ++j) {
@@ -462,7 +474,7 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
       for (int r = 0; r < LN::EPT; ++r) v[r] = kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M);
       if (j + 1 < a.n_comp) {
 #pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(a.ks[j + 1], l, LN::out_idx(t, r), LN::M);
+        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<TC>(a.ks[j + 1], l, LN::out_idx(t, r), LN::M, r);
       }
     }
     fft_line<LN, true>(v, t, xb, tws);
@@ -475,6 +487,29 @@ __global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_
     }
   }
   tmem_free_cta(tbase, TC::COLS);
+}
+
+// Register-order copy of a folded real/imaginary spectrum for the column
+// kernel configuration CFG (see KSpec::perm).  One thread per output value.
+template <class CFG>
+__global__ void spectrum_perm_kernel(const double* __restrict__ re, int64_t ld, int64_t nlines, int odd0,
+                                     double* __restrict__ kp, int64_t total) {
+  using LN = typename CFG::LN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int tid = (int)(i % CFG::NT);
+    const int64_t rest = i / CFG::NT;
+    const int r = (int)(rest % LN::EPT);
+    const int64_t b = rest / LN::EPT;
+    const int64_t l = b * CFG::LPC + CFG::line_of(tid);
+    const int k0 = LN::out_idx(CFG::t_of(tid), r);
+    const bool hi = k0 > (LN::M >> 1);
+    double v = 0.0;
+    if (l < nlines) {
+      v = re[(int64_t)(hi ? LN::M - k0 : k0) * ld + l];
+      if (odd0 && hi) v = -v;
+    }
+    kp[i] = v;
+  }
 }
 
 // Strided batched c2c lines (3D axis 1, both directions).  Line l of component

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 
 #include "launch.cuh"
@@ -38,6 +39,32 @@ int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
   if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
   k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, smem, st>>>(a);
   CK(cudaGetLastError());
+  return EIK_OK;
+}
+
+// Register-order spectrum for the column kernel launch_col picks at length 2^L
+// for real spectra (COMPS / SUM).  kp == nullptr: only report the size.
+template <class C>
+int permute_t(const double* re, int64_t ld, int64_t nlines, int odd0, double* kp, int64_t* elems, cudaStream_t st) {
+  const int64_t tiles = (nlines + C::LPC - 1) / C::LPC;
+  const int64_t total = tiles * C::LN::EPT * C::NT;
+  *elems = total;
+  if (!kp || total == 0) return EIK_OK;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 64);
+  spectrum_perm_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(re, ld, nlines, odd0, kp, total);
+  CK(cudaGetLastError());
+  return EIK_OK;
+}
+
+int launch_spectrum_perm(int L, const double* re, int64_t ld, int64_t nlines, int odd0, double* kp, int64_t* elems,
+                         cudaStream_t st) {
+#define EIK_PERM(Lc)                                                                               \
+  if constexpr (Lc >= 9) {                                                                         \
+    if (use_tmem()) return permute_t<TmCfg<Lc>>(re, ld, nlines, odd0, kp, elems, st);              \
+  }                                                                                                \
+  return permute_t<ColCfg<Lc>>(re, ld, nlines, odd0, kp, elems, st)
+  EIK_SWITCH_L(L, EIK_PERM);
+#undef EIK_PERM
   return EIK_OK;
 }
 

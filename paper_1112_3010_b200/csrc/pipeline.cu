@@ -100,6 +100,7 @@ struct KDev {
   int odd0 = 0;
   double sign = 1.0;
   DevBuf buf;  // folded real/imag spectrum [(M0/2+1) x lines]
+  DevBuf kp;   // register-order copy for the 2-D column kernels (KSpec::perm), or empty
 };
 
 }  // namespace
@@ -283,6 +284,14 @@ int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, in
   }
   int rc = spectrum_of(p, g, k->imag ? SPEC_IMAG_T : SPEC_REAL_T, k->buf.as<double>(), nullptr, work, st);
   if (rc) return rc;
+  if (p->D == 2 && p->ks_l0 == 0 && p->ks_lines == p->lines) {
+    int64_t elems = 0;
+    if ((rc = launch_spectrum_perm(p->L[0], nullptr, 0, p->ks_lines, 0, nullptr, &elems, st))) return rc;
+    CK(k->kp.ensure(elems * sizeof(double)));
+    if ((rc = launch_spectrum_perm(p->L[0], k->buf.as<double>(), p->ks_lines, p->ks_lines, k->odd0,
+                                   k->kp.as<double>(), &elems, st)))
+      return rc;
+  }
   v.push_back(std::move(k));
   return EIK_OK;
 }
@@ -293,6 +302,10 @@ KSpec kspec_of(const eik_plan* p, const KDev& k) {
   s.ld = p->ks_lines;
   s.imag = k.imag;
   s.odd0 = k.odd0;
+  if (k.kp.bytes) {
+    s.perm = k.kp.as<double>();
+    s.odd0 = 0;
+  }
   return s;
 }
 
@@ -444,6 +457,10 @@ int set_components(const eik_plan* p, bool sign_group, const Roles& r, ColArgs& 
   auto ks = [&](const KDev& k) {
     KSpec s = kspec_of(p, k);
     s.re += k1_offset_lines - p->ks_l0;  // k1-slab: lines [k1b*H, ...) of the global layout
+    if (k1_offset_lines != p->ks_l0) {  // the register-order copy covers the plan's own lines only
+      s.perm = nullptr;
+      s.odd0 = k.odd0;
+    }
     return s;
   };
   if (sign_group) {
