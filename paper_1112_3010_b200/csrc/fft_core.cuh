@@ -398,7 +398,7 @@ struct Line4K {
   static constexpr bool FOUR_STEP = true;
   static constexpr int L = 12, E = 16, M = 4096, EPT = 16, TPL = 256, R0 = 16, RL = 16, NST = 3;
   static constexpr int PITCH = 272;
-  static constexpr int SMEM = 16 * PITCH;
+  static constexpr int SMEM = 16 * PITCH + 4;  // line stride: == 4 (mod 8) so lane-interleaved lines miss each other's banks
   static constexpr int TWQ = tpos_size(M >> 2);
   static constexpr bool INV_SHARES = true;
   static constexpr int ST_SIZE = 16 * 15;  // W_256^{j a}, j < 16, 1 <= a < 16

@@ -372,13 +372,25 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 #ifndef EIK_FOUR_STEP
 #define EIK_FOUR_STEP 1
 #endif
-template <int L>
+#ifndef EIK_F4K_LPC
+#define EIK_F4K_LPC 2
+#endif
+// Four-step 4096-point lines of the multi-component (COMPS) kernel: EIK_F4K_LPC
+// lines per CTA, interleaved by lane parity, so warp loads/stores cover two
+// adjacent columns (one CTA per SM).  The SUM kernel (sign group: two forward
+// transforms, one inverse) keeps one line per CTA: measured faster there.
+__host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
+  return (L == 12 && EIK_FOUR_STEP && OUT == OUT_COMPS) ? EIK_F4K_LPC : 1;
+}
+template <int L, int LPCX = 1>
 struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
-  static constexpr int NT = TPL0 > 256 ? TPL0 : 256;
+  static constexpr bool F4K = (L == 12 && EIK_FOUR_STEP);
+  static constexpr int NT = F4K ? 256 * LPCX : (TPL0 > 256 ? TPL0 : 256);
   static constexpr int LPC = NT / TPL0;
+  static constexpr int MINB = NT >= 512 ? 1 : 2;
   static constexpr int IL = col_il(LPC);
-  using LN = std::conditional_t<(L == 12 && EIK_FOUR_STEP), Line4K, PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>;
+  using LN = std::conditional_t<F4K, Line4K, PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>;
   using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
@@ -393,8 +405,9 @@ struct TmCfg {
 };
 
 template <int L, int IN, int OUT, bool HALF>
-__global__ void __launch_bounds__(TmCfg<L>::NT, 2) col_tmem_kernel(const __grid_constant__ ColArgs a) {
-  using TC = TmCfg<L>;
+__global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpcx(L, OUT)>::MINB)
+    col_tmem_kernel(const __grid_constant__ ColArgs a) {
+  using TC = TmCfg<L, tm_lpcx(L, OUT)>;
   using LN = typename TC::LN;
   constexpr int LPC = TC::LPC;
   extern __shared__ double2 smem[];

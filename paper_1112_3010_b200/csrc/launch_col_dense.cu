@@ -14,7 +14,7 @@ static bool use_tmem() {
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
-  using C = TmCfg<L>;
+  using C = TmCfg<L, tm_lpcx(L, OUT)>;
   auto k = col_tmem_kernel<L, IN, OUT, HALF>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
@@ -56,12 +56,14 @@ int permute_t(const double* re, int64_t ld, int64_t nlines, int odd0, double* kp
   return EIK_OK;
 }
 
-int launch_spectrum_perm(int L, const double* re, int64_t ld, int64_t nlines, int odd0, double* kp, int64_t* elems,
-                         cudaStream_t st) {
-#define EIK_PERM(Lc)                                                                               \
-  if constexpr (Lc >= 9) {                                                                         \
-    if (use_tmem()) return permute_t<TmCfg<Lc>>(re, ld, nlines, odd0, kp, elems, st);              \
-  }                                                                                                \
+int launch_spectrum_perm(int L, bool sum, const double* re, int64_t ld, int64_t nlines, int odd0, double* kp,
+                         int64_t* elems, cudaStream_t st) {
+#define EIK_PERM(Lc)                                                                                     \
+  if constexpr (Lc >= 9) {                                                                               \
+    if (use_tmem())                                                                                      \
+      return sum ? permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_SUM)>>(re, ld, nlines, odd0, kp, elems, st)       \
+                 : permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_COMPS)>>(re, ld, nlines, odd0, kp, elems, st);    \
+  }                                                                                                      \
   return permute_t<ColCfg<Lc>>(re, ld, nlines, odd0, kp, elems, st)
   EIK_SWITCH_L(L, EIK_PERM);
 #undef EIK_PERM

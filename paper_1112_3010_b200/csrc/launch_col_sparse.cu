@@ -13,7 +13,7 @@ static bool use_tmem() {
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
-  using C = TmCfg<L>;
+  using C = TmCfg<L, tm_lpcx(L, OUT)>;
   auto k = col_tmem_kernel<L, IN, OUT, HALF>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;

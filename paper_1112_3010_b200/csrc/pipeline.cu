@@ -286,9 +286,10 @@ int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, in
   if (rc) return rc;
   if (p->D == 2 && p->ks_l0 == 0 && p->ks_lines == p->lines) {
     int64_t elems = 0;
-    if ((rc = launch_spectrum_perm(p->L[0], nullptr, 0, p->ks_lines, 0, nullptr, &elems, st))) return rc;
+    const bool sum = &v == &p->ksign;  // the sign group runs the SUM column kernel
+    if ((rc = launch_spectrum_perm(p->L[0], sum, nullptr, 0, p->ks_lines, 0, nullptr, &elems, st))) return rc;
     CK(k->kp.ensure(elems * sizeof(double)));
-    if ((rc = launch_spectrum_perm(p->L[0], k->buf.as<double>(), p->ks_lines, p->ks_lines, k->odd0,
+    if ((rc = launch_spectrum_perm(p->L[0], sum, k->buf.as<double>(), p->ks_lines, p->ks_lines, k->odd0,
                                    k->kp.as<double>(), &elems, st)))
       return rc;
   }
