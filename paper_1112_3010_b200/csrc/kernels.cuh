@@ -23,6 +23,7 @@
 #pragma once
 #include "fft_core.cuh"
 #include "tmem.cuh"
+#include "bulk.cuh"
 
 #include <type_traits>
 
@@ -122,13 +123,23 @@ struct RowCfg {
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
   static constexpr int NBUF = (LH <= 10 && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
   using XB = XBuf<NBUF, group_sync(1, LPC, LN::TPL), LN::TPL>;  // row kernels are line-major
-  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
+  static constexpr size_t BASE_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
   // resident CTAs per SM requested from the register allocator (128 threads:
   // 4 CTAs = 16 warps at <= 128 registers)
 #ifndef EIK_ROW_MINB128
 #define EIK_ROW_MINB128 4
 #endif
   static constexpr int MINB = (NT <= 128 && LN::EPT <= 8) ? EIK_ROW_MINB128 : (NT <= 256 ? 2 : 1);
+  // Row prefetch: each line's next spectral row (M/2+1 complex values,
+  // contiguous) is bulk-copied into shared memory while the current one is
+  // transformed, where it fits next to MINB resident CTAs.
+#ifndef EIK_ROW_FEED
+#define EIK_ROW_FEED 1
+#endif
+  static constexpr size_t FEED_BYTES = (size_t)LPC * (LN::M + 1) * sizeof(double2) + LPC * sizeof(uint64_t);
+  // (long rows only: measured neutral-to-slower for multi-line CTAs, C3 / C5)
+  static constexpr bool FEED = EIK_ROW_FEED && LN::TPL >= 128 && (BASE_BYTES + FEED_BYTES + 16) * MINB <= 227 * 1024;
+  static constexpr size_t SMEM_BYTES = BASE_BYTES + (FEED ? FEED_BYTES + 16 : 0);
 };
 
 // Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
@@ -195,11 +206,19 @@ __device__ __forceinline__ double kload(const KSpec& k, int64_t l, int k0, int M
   const bool hi = k0 > (M0 >> 1);
   return __ldg(k.re + (int64_t)(hi ? M0 - k0 : k0) * k.ld + l);
 }
-// kload for a kernel of configuration CFG (register r of this thread)
+// All EPT kernel-spectrum values of this thread for a kernel of configuration
+// CFG (one uniform branch on the layout, outside the unrolled loads).
 template <class CFG>
-__device__ __forceinline__ double kload_c(const KSpec& k, int64_t l, int k0, int M0, int r) {
-  if (k.perm) return __ldg(k.perm + ((int64_t)blockIdx.x * CFG::LN::EPT + r) * CFG::NT + threadIdx.x);
-  return kload(k, l, k0, M0);
+__device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpec& k, int64_t l, int t) {
+  using LN = typename CFG::LN;
+  if (k.perm) {
+    const double* __restrict__ src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NT + threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) kn[r] = __ldg(src + r * CFG::NT);
+  } else {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(k, l, LN::out_idx(t, r), LN::M);
+  }
 }
 __device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0) {
   if (k.odd0 && k0 > (M0 >> 1)) v = -v;
@@ -287,8 +306,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     const bool real_ks = a.ks[0].cplx == nullptr;
     double kn[LN::EPT];  // next component's kernel spectrum, prefetched
     if (real_ks && valid) {
-#pragma unroll
-      for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<ColCfg<L>>(a.ks[0], l, LN::out_idx(t, r), LN::M, r);
+      kload_all<ColCfg<L>>(kn, a.ks[0], l, t);
     }
 #pragma unroll 1
     for (int j = 0; j < a.n_comp; ++j) {
@@ -297,8 +315,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M) : v[r];
         if (j + 1 < a.n_comp && valid) {
-#pragma unroll
-          for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<ColCfg<L>>(a.ks[j + 1], l, LN::out_idx(t, r), LN::M, r);
+          kload_all<ColCfg<L>>(kn, a.ks[j + 1], l, t);
         }
       } else {
 #pragma unroll
@@ -322,8 +339,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       const bool real_ks = a.ks[i].cplx == nullptr;
       double kn[LN::EPT];  // this input's kernel spectrum, loaded before its transform
       if (real_ks && valid) {
-#pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<ColCfg<L>>(a.ks[i], l, LN::out_idx(t, r), LN::M, r);
+        kload_all<ColCfg<L>>(kn, a.ks[i], l, t);
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
@@ -442,8 +458,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     for (int i = 0; i < a.n_in; ++i) {
       double kn[LN::EPT];
       if (valid) {
-#pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<TC>(a.ks[i], l, LN::out_idx(t, r), LN::M, r);
+        kload_all<TC>(kn, a.ks[i], l, t);
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
@@ -476,8 +491,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   tmem_put(ta, v);
   double kn[LN::EPT];
   if (valid) {
-#pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<TC>(a.ks[0], l, LN::out_idx(t, r), LN::M, r);
+    kload_all<TC>(kn, a.ks[0], l, t);
   }
 #pragma unroll 1
   for (int j = 0; j < a.n_comp; ++j) {
@@ -486,8 +500,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) v[r] = kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M);
       if (j + 1 < a.n_comp) {
-#pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) kn[r] = kload_c<TC>(a.ks[j + 1], l, LN::out_idx(t, r), LN::M, r);
+        kload_all<TC>(kn, a.ks[j + 1], l, t);
       }
     }
     fft_line<LN, true>(v, t, xb, tws);
@@ -764,17 +777,29 @@ struct RowArgs {
   int lmax;
 };
 
-template <class LN, class XB>
-__device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* __restrict__ X, int t,
-                                         XB& xb, const double2* twq, const double2* sts, bool valid) {
+// Per-line prefetch state of the row pass (RowCfg::FEED): xs holds the row
+// being consumed / in flight; `bar` completes when it has landed.
+struct RowFeed {
+  double2* xs;
+  uint64_t* bar;
+  uint32_t phase;
+  int next;   // next component to fetch
+  int total;  // components this CTA processes, in order 0..total-1
+};
+
+// c2r pre-twist of one half-spectrum row (X[k], k in [0, M]) into the complex
+// line z the inverse transform consumes; src is global or a shared-memory copy.
+template <class LN>
+__device__ __forceinline__ void c2r_twist(double2 (&z)[LN::EPT], const double2* src, int t, const double2* twq,
+                                          bool valid) {
   constexpr int MH = LN::M;
   constexpr int LQ = LN::L + 1;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
     const int k = LN::out_idx(t, r);
     if (valid) {
-      const double2 xa = X[k];
-      const double2 xb = X[MH - k];  // conj taken below
+      const double2 xa = src[k];
+      const double2 xb = src[MH - k];  // conj taken below
       const double2 e = make_double2(xa.x + xb.x, xa.y - xb.y);   // X[k] + conj X[MH-k]
       const double2 d = make_double2(xa.x - xb.x, xa.y + xb.y);   // X[k] - conj X[MH-k]
       const double2 o = cmulc(d, twq_get(twq, LQ, k));            // * W_M^{-k}
@@ -783,7 +808,6 @@ __device__ __forceinline__ void c2r_line(double2 (&z)[LN::EPT], const double2* _
       z[r] = make_double2(0.0, 0.0);
     }
   }
-  fft_line<LN, true>(z, t, xb, TwSrc{sts, twq, LN::L + 1, 0u});
 }
 
 template <int LH>
@@ -801,14 +825,52 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + RC::TWQ;
-  twq_fill(twq, LH + 1, a.tw, a.lmax);
-  st_fill<LN>(sts, a.tw, a.lmax);
-  __syncthreads();
   const int64_t rb = valid ? row % a.rows_a : 0;
   const int64_t roff = item * a.comp_item +
                        (valid ? (row / a.rows_a) * a.stride_a + (rb >> a.split_shift) * a.split_stride +
                                     (rb & ((int64_t(1) << a.split_shift) - 1)) * a.stride_b
                               : 0);
+  constexpr uint32_t ROW_BYTES = (LN::M + 1) * sizeof(double2);
+  RowFeed fd{nullptr, nullptr, 0u, 0, a.n_raw > 0 ? a.n_raw : a.n_comp};
+  auto feed_issue = [&]() {  // thread 0 of the line: start fetching component fd.next
+    if (RC::FEED && t == 0 && valid && fd.next < fd.total) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(fd.bar, ROW_BYTES);
+      bulk_g2s(fd.xs, a.comp[fd.next] + roff, ROW_BYTES, fd.bar);
+    }
+    ++fd.next;
+  };
+  if constexpr (RC::FEED) {
+    char* fb = reinterpret_cast<char*>(smem) + ((RC::BASE_BYTES + 15) & ~size_t(15));
+    fd.xs = reinterpret_cast<double2*>(fb) + (size_t)line * (LN::M + 1);
+    fd.bar = reinterpret_cast<uint64_t*>(fb + (size_t)LPC * ROW_BYTES) + line;
+    if (t == 0) {
+      mbar_init(fd.bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    feed_issue();
+  }
+  // the current component's row: from the prefetch buffer (waits for it) or global
+  auto row_src = [&]() -> const double2* {
+    if constexpr (RC::FEED) {
+      if (valid) mbar_wait(fd.bar, fd.phase);
+      fd.phase ^= 1u;
+      return fd.xs;
+    } else {
+      return nullptr;
+    }
+  };
+  // after the twist has read the row: every thread of the line is past it, refill
+  auto feed_next = [&]() {
+    if constexpr (RC::FEED) {
+      xb.sync();
+      feed_issue();
+    }
+  };
+  twq_fill(twq, LH + 1, a.tw, a.lmax);
+  st_fill<LN>(sts, a.tw, a.lmax);
+  __syncthreads();
   const int64_t obase = item * a.N + row * a.n_out;
   const bool even = (a.n_out & 1) == 0;
 
@@ -828,9 +890,16 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
 
   double2 phi[E], sg[3][E];
   double2 z[E];
+  // inverse real transform of component c's row into z (prefetching the next row)
+  auto row_c2r = [&](const double2* X) {
+    const double2* xs = row_src();
+    c2r_twist<LN>(z, xs ? xs : X, t, twq, valid);
+    feed_next();
+    fft_line<LN, true>(z, t, xb, TwSrc{sts, twq, LN::L + 1, 0u});
+  };
   unsigned cnt = 0;
   if (a.c_phi >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_phi] + roff, t, xb, twq, sts, valid);
+    row_c2r(a.comp[a.c_phi] + roff);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -852,7 +921,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   if (a.c_grad >= 0) {
 #pragma unroll 1
     for (int d = 0; d < a.ngrad; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_grad + d] + roff, t, xb, twq, sts, valid);
+      row_c2r(a.comp[a.c_grad + d] + roff);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -865,7 +934,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   if (a.c_hess >= 0) {
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
-      c2r_line<LN>(z, a.comp[a.c_hess + d] + roff, t, xb, twq, sts, valid);
+      row_c2r(a.comp[a.c_hess + d] + roff);
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
@@ -879,7 +948,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
     }
   }
   if (a.c_sign >= 0) {
-    c2r_line<LN>(z, a.comp[a.c_sign] + roff, t, xb, twq, sts, valid);
+    row_c2r(a.comp[a.c_sign] + roff);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
       if (!active(r)) continue;
@@ -901,7 +970,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   }
 #pragma unroll 1
   for (int j = 0; j < a.n_raw; ++j) {
-    c2r_line<LN>(z, a.comp[j] + roff, t, xb, twq, sts, valid);
+    row_c2r(a.comp[j] + roff);
     const double tj = a.raw_tau[j];  // tau sweep: raw_tau > 0 turns phi_j into S_j = -tau_j log phi_j
 #pragma unroll
     for (int r = 0; r < E; ++r) {
