@@ -89,6 +89,8 @@ def algorithmic_bytes(plan_info, w, batch):
     row = n_c*16*c0*H + (8*n_f64_out + n_u8_out)*N.
     """
     grid = w["grid"]
+    if len(grid.counts) == 3:
+        return algorithmic_bytes_3d(plan_info, w, batch)
     if len(grid.counts) != 2:
         return {}
     c0, c1 = grid.counts
@@ -105,6 +107,28 @@ def algorithmic_bytes(plan_info, w, batch):
     n_f64 = 1 + (dim if w.get("grad") else 0) + (3 if w.get("hess") else 0) + (1 if w.get("sign") is not None else 0)
     n_u8 = 1 if w.get("sign") is not None else 0
     out["row"] = batch * (n_c * 16 * c0 * H + (8 * n_f64 + n_u8) * c0 * c1)
+    return out
+
+
+def algorithmic_bytes_3d(plan_info, w, batch):
+    """3-D pass model (c0 x c1 x c2 grid, M = 2c, H = M2/2+1).
+
+    col   = impulse rows T (16*c0*c1*H written + read) + V (16*c0*M1*H written
+            by the axis-1 forward, read by the axis-0 pass) + kernel spectra
+            n_k*8*(M0/2+1)*M1*H + components n_c*16*c0*M1*H written;
+    lines = n_c*16*c0*M1*H read + n_c*16*c0*c1*H written (axis-1 inverse);
+    row   = n_c*16*c0*c1*H read + (8*n_f64_out + n_u8_out)*N written.
+    """
+    c0, c1, c2 = w["grid"].counts
+    M0, M1, M2 = plan_info["padded"][:3]
+    H = M2 // 2 + 1
+    n_c = 1 + (3 if w.get("grad") else 0)
+    ks = (M0 // 2 + 1) * M1 * H * 8
+    plane = 16 * c0 * M1 * H
+    slab = 16 * c0 * c1 * H
+    out = {"col": batch * (2 * slab + 2 * plane + n_c * plane) + n_c * ks,
+           "lines": batch * n_c * (plane + slab),
+           "row": batch * (n_c * slab + 8 * n_c * c0 * c1 * c2)}
     return out
 
 

@@ -1014,20 +1014,19 @@ struct RowDftArgs {
 };
 
 constexpr int ROWDFT_NT = 256;
-constexpr int ROWDFT_NF = 16;     // max frequencies per thread
+constexpr int ROWDFT_NF = 16;     // max frequencies per thread (H <= ROWDFT_NF * ROWDFT_NT)
 constexpr int ROWDFT_STAGE = 1536;  // staged points per CTA and chunk (<= 42 KB of shared memory)
 
-// Threads per row: enough for H frequencies at <= 16 each, power of two, <= 256.
-__host__ __device__ constexpr int rowdft_tpr(int64_t H) {
-  int t = 1;
-  while (t < 256 && (int64_t)t * ROWDFT_NF < H) t <<= 1;
-  return t;
-}
+// Frequencies k in [0, M/2) are spread as k = tl + q * tpr, q < NF, over tpr
+// threads per row; the Nyquist term k = M/2 is one extra accumulator of the
+// row's thread 0.  NF = 8 (or M/2 below 16 points: 1, 2, 4), so tpr = M/16 <= 256.
+__host__ __device__ constexpr int rowdft_nf(int64_t H) { return H - 1 >= 8 ? 8 : (int)(H - 1); }
+__host__ __device__ constexpr int rowdft_tpr(int64_t H) { return (int)((H - 1) / rowdft_nf(H)); }
 
-template <int NIN>
+template <int NIN, int NF>
 __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_constant__ RowDftArgs a) {
   extern __shared__ double rowdft_smem[];
-  const int tpr = rowdft_tpr(a.H);
+  const int tpr = (int)((a.H - 1) / NF);
   const int rpb = ROWDFT_NT / tpr;
   const int rl = threadIdx.x / tpr, tl = threadIdx.x % tpr;
   const int ROWDFT_CHUNK = ROWDFT_STAGE / rpb;  // per row
@@ -1039,12 +1038,15 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   double* ws = rowdft_smem;
   const int64_t grow = item * a.rows_per_item + (valid ? row : 0);
   const int64_t p0 = valid ? __ldg(a.rowptr + grow) : 0, p1 = valid ? __ldg(a.rowptr + grow + 1) : 0;
-  const int nk = (int)((a.H + tpr - 1) / tpr);
-  double2 acc[NIN][ROWDFT_NF];
+  const int nyq_shift = a.last_shift;  // W^{(col * M/2) mod M}: index 0 or M/2 of the M-point table
+  const int64_t half = a.H - 1;
+  double2 acc[NIN][NF], nyq[NIN];
 #pragma unroll
-  for (int i = 0; i < NIN; ++i)
+  for (int i = 0; i < NIN; ++i) {
+    nyq[i] = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < ROWDFT_NF; ++q) acc[i][q] = make_double2(0.0, 0.0);
+    for (int q = 0; q < NF; ++q) acc[i][q] = make_double2(0.0, 0.0);
+  }
   // rows of one CTA may differ in length: loop to the CTA's longest row
   __shared__ int s_maxlen;
   if (threadIdx.x == 0) s_maxlen = 0;
@@ -1069,15 +1071,21 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
 #pragma unroll
       for (int i = 0; i < NIN; ++i) wv[i] = ws[(i * rpb + rl) * ROWDFT_CHUNK + p];
 #pragma unroll
-      for (int q = 0; q < ROWDFT_NF; ++q) {
+      for (int q = 0; q < NF; ++q) {
         const int64_t k = tl + (int64_t)q * tpr;
-        if (q < nk && k < a.H) {
-          const double2 t = __ldg(a.tw + ((int)((col * k) & a.last_mask) << a.last_shift));
+        const double2 t = __ldg(a.tw + ((int)((col * k) & a.last_mask) << a.last_shift));
 #pragma unroll
-          for (int i = 0; i < NIN; ++i) {
-            acc[i][q].x = fma(wv[i], t.x, acc[i][q].x);
-            acc[i][q].y = fma(wv[i], t.y, acc[i][q].y);
-          }
+        for (int i = 0; i < NIN; ++i) {
+          acc[i][q].x = fma(wv[i], t.x, acc[i][q].x);
+          acc[i][q].y = fma(wv[i], t.y, acc[i][q].y);
+        }
+      }
+      if (tl == 0) {
+        const double2 t = __ldg(a.tw + ((int)((col * half) & a.last_mask) << nyq_shift));
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) {
+          nyq[i].x = fma(wv[i], t.x, nyq[i].x);
+          nyq[i].y = fma(wv[i], t.y, nyq[i].y);
         }
       }
     }
@@ -1087,11 +1095,27 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   for (int i = 0; i < NIN; ++i) {
     double2* dst = a.out[i] + item * a.out_item + row * a.H;
 #pragma unroll
-    for (int q = 0; q < ROWDFT_NF; ++q) {
-      const int64_t k = tl + (int64_t)q * tpr;
-      if (q < nk && k < a.H) dst[k] = acc[i][q];
-    }
+    for (int q = 0; q < NF; ++q) dst[tl + (int64_t)q * tpr] = acc[i][q];
+    if (tl == 0) dst[half] = nyq[i];
   }
+}
+
+// Launch the impulse DFT for n_in inputs over `rows` rows of `items` items.
+inline cudaError_t launch_impulse_rows(const RowDftArgs& ra, int n_in, int64_t rows, int64_t items, cudaStream_t st) {
+  const int nf = rowdft_nf(ra.H), tpr = rowdft_tpr(ra.H), rpb = ROWDFT_NT / tpr;
+  const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
+  const dim3 grid((unsigned)((rows + rpb - 1) / rpb), (unsigned)items);
+#define EIK_ROWDFT_NF(NI, F) \
+  if (n_in == NI && nf == F) impulse_rows_kernel<NI, F><<<grid, ROWDFT_NT, smem, st>>>(ra)
+#define EIK_ROWDFT_NI(NI) \
+  EIK_ROWDFT_NF(NI, 1); else EIK_ROWDFT_NF(NI, 2); else EIK_ROWDFT_NF(NI, 4); else EIK_ROWDFT_NF(NI, 8)
+  EIK_ROWDFT_NI(1);
+  else EIK_ROWDFT_NI(2);
+  else EIK_ROWDFT_NI(3);
+  else return cudaErrorInvalidValue;
+#undef EIK_ROWDFT_NI
+#undef EIK_ROWDFT_NF
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

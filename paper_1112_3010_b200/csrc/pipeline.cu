@@ -515,15 +515,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     ra.last_shift = p->lmax - p->L[1];
     ra.last_mask = p->M[1] - 1;
     ra.tw = p->tw.as<double2>();
-    {
-      const int tpr = rowdft_tpr(p->H), rpb = ROWDFT_NT / tpr;
-      const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
-      const dim3 grid((unsigned)((p->c[0] + rpb - 1) / rpb), (unsigned)B);
-      if (n_in == 1) impulse_rows_kernel<1><<<grid, ROWDFT_NT, smem, st>>>(ra);
-      else if (n_in == 2) impulse_rows_kernel<2><<<grid, ROWDFT_NT, smem, st>>>(ra);
-      else impulse_rows_kernel<3><<<grid, ROWDFT_NT, smem, st>>>(ra);
-      CK(cudaGetLastError());
-    }
+    CK(launch_impulse_rows(ra, n_in, p->c[0], B, st));
     ColArgs a = col_defaults(p);
     a.nlines = p->H;
     a.n_valid = p->c[0];
@@ -592,12 +584,7 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
     ra.last_shift = p->lmax - p->L[2];
     ra.last_mask = p->M[2] - 1;
     ra.tw = p->tw.as<double2>();
-    const int tpr = rowdft_tpr(H), rpb = ROWDFT_NT / tpr;
-    const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
-    const dim3 grid((unsigned)((c0loc * c1 + rpb - 1) / rpb), (unsigned)B);
-    if (n_in == 1) impulse_rows_kernel<1><<<grid, ROWDFT_NT, smem, st>>>(ra);
-    else impulse_rows_kernel<3><<<grid, ROWDFT_NT, smem, st>>>(ra);
-    CK(cudaGetLastError());
+    CK(launch_impulse_rows(ra, n_in, c0loc * c1, B, st));
     LinesArgs la = lines_defaults(p);
     for (int i = 0; i < n_in; ++i) { la.in[i] = ra.out[i]; la.out[i] = V[i]; }
     la.nlines = B * c0loc * H;
@@ -1127,12 +1114,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
   rd.last_mask = p->M[1] - 1;
   rd.tw = p->tw.as<double2>();
   if (p->H > (int64_t)ROWDFT_NF * ROWDFT_NT) return fail(EIK_EVALIDATION, "last axis too long for the sweep");
-  {
-    const int tpr = rowdft_tpr(p->H), rpb = ROWDFT_NT / tpr;
-    const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (sizeof(double) + sizeof(int32_t));
-    impulse_rows_kernel<1><<<dim3((unsigned)((p->c[0] + rpb - 1) / rpb), 1), ROWDFT_NT, smem, st>>>(rd);
-    CK(cudaGetLastError());
-  }
+  CK(launch_impulse_rows(rd, 1, p->c[0], 1, st));
   double scale = 1.0;
   for (int a = 0; a < p->D; ++a) scale /= (double)p->M[a];
   for (int t0 = 0; t0 < nt; t0 += MAXC) {
