@@ -38,7 +38,8 @@ CONFIG_TEXT = {
     "TS": "tau sweep (SURVEY 8(f) rank 1): C2's 2048^2 delta_Y, S for 9 taus 0.5..4.5 from one transform "
           "(metric counts grid points x taus)",
     "C4": "3D 1024^3 perturbed icosphere (501,762 vertices, vector-area normals), tau=0.75: S + grad S + degree sign; "
-          "slab-decomposed, NCCL all-to-all (512^3 with scaled surface on fewer than 4 GPUs: memory)",
+          "slab-decomposed, exchange fused into the passes as NVLink peer stores (--exchange nccl: NCCL "
+          "all-to-all) (512^3 with scaled surface on fewer than 4 GPUs: memory)",
 }
 
 
@@ -52,6 +53,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--items", type=int, default=512, help="C5 batch size (whole job)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="C4 slab exchange: fused peer stores (p2p) or NCCL all_to_all_single")
     return ap.parse_args()
 
 
@@ -560,18 +563,32 @@ def bench_c4(a):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1112_3010_b200 import workloads as wl
-    from paper_1112_3010_b200.slab import CudaSlabExecutor, local_nodes, nccl_exchange, run_rank
+    from paper_1112_3010_b200.slab import (CudaSlabExecutor, connect_p2p, local_nodes, nccl_exchange, run_rank,
+                                           run_rank_p2p, stream_barrier)
 
     n = 1024 if world >= 4 else 512
     d = wl.c4(a.seed, n=n)
     grid = d["grid"]
     t_plan = time.perf_counter()
-    ex = CudaSlabExecutor(grid, d["tau"], world, rank, grad=True, sign=True, device=local)
+    p2p = a.exchange == "p2p"
+    ex = CudaSlabExecutor(grid, d["tau"], world, rank, grad=True, sign=True, device=local, p2p=p2p)
     t_plan = time.perf_counter() - t_plan
     ln, _ = local_nodes(d["nodes"], ex.layout)
     lsn, lsw = local_nodes(d["sign_nodes"], ex.layout, d["sign_weights"])
     ln_d, lsn_d, lsw_d = (torch.as_tensor(x, device=dev) for x in (ln, lsn, lsw))
-    if dist:
+    if p2p:
+        # exchanges fused into the passes (peer stores into the owners' arenas)
+        if dist:
+            connect_p2p(ex, dist)
+            barrier = stream_barrier(dist, dev)
+        else:
+            ex.plan.slab_p2p_connect(peer_arenas=[ex.arena])
+            barrier = lambda: None  # noqa: E731
+
+        def run_rank(ex_, _exchange, *args):
+            return run_rank_p2p(ex_, barrier, *args)
+        exchange = None
+    elif dist:
         exchange = nccl_exchange(dist)
     else:
         def exchange(send, recv):
@@ -628,8 +645,10 @@ def bench_c4(a):
             "data": "synthetic (seeded perturbed icosphere, workloads.c4)",
             "config": {"workload": "C4" if n == 1024 else "C4@512^3", "desc": CONFIG_TEXT["C4"], "grid": list(grid.counts),
                        "padded": list(L.padded), "vertices": int(d["vertices"].shape[0]),
-                       "nodes": int(d["nodes"].size), "parallelism": f"slab x{world} (NCCL all-to-all)",
-                       "all_to_all_bytes_per_step": int(9 * 16 * L.buf * world) if world > 1 else 0,
+                       "nodes": int(d["nodes"].size),
+                       "parallelism": f"slab x{world} " + ("(exchange fused into the passes: NVLink peer stores, "
+                                                          "2 stream barriers)" if p2p else "(NCCL all-to-all)"),
+                       "exchange_bytes_per_step": int(9 * 16 * L.buf * world * (world - 1) / world) if world > 1 else 0,
                        "l2": "working set >> L2", "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": grid.num_nodes * ke / (e2e_ms / 1e3), "unit": "grid_points/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ke},

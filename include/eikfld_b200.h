@@ -53,6 +53,7 @@ extern "C" {
 #define EIK_CHECK_UNDERFLOW 0x8u   /* sync, and return EIK_EUNDERFLOW if any phi <= 0
                                       (R/convolution.py:378-388 assert_positive) */
 #define EIK_PROFILE 0x10u          /* record CUDA events around each pass (see eik_pass_times) */
+#define EIK_SLAB_P2P 0x20u         /* slab passes: exchange through peer arenas (eik_slab_p2p_*) */
 
 /* pass ids reported by eik_pass_times */
 #define EIK_PASS_PREP 0     /* node validation + per-row CSR */
@@ -143,6 +144,27 @@ int eik_slab_axis0(eik_plan* plan, int group, double* const* v_in, int64_t k1_be
                    double* const* w_out, uint32_t flags, void* stream);
 int eik_slab_finish(eik_plan* plan, double* const* w, int64_t c0_local, int64_t ks, const eik_outputs* out,
                     uint32_t flags, void* stream);
+
+/* Peer-to-peer slab exchange: the two all-to-alls fused into the passes.
+ * Each rank's plan owns one device arena of (4 + n_comp) slots, each slot
+ * G * c0_local * ks * H2 complex in the receive layout [G src][c0_local][ks][H2]
+ * (V slots: 0 = delta_Y, 1..3 = flux fields; then one W slot per component).
+ * With EIK_SLAB_P2P, eik_slab_planes stores its k1-slab blocks straight into
+ * the owning rank's V slots and eik_slab_axis0 stores its rows straight into
+ * the owning rank's W slots (NVLink stores through peer pointers, overlapped
+ * with the transforms); both read / eik_slab_finish reads the own arena and
+ * ignore their buffer arguments.  No data collective remains: the caller
+ * orders the ranks with a stream-ordered barrier after each planes pass and
+ * after the last axis-0 pass (replacing the reference-free NCCL schedule's
+ * one all-to-all per buffer).  c0_local must be a power of two; G <= 8.
+ *   eik_slab_p2p_init     allocate the arena; return its device pointer, size
+ *                         and (ipc_handle != NULL) its 64-byte CUDA IPC handle.
+ *   eik_slab_p2p_connect  peer arenas by device pointer (same process: the
+ *                         single-GPU emulation) or by IPC handle (world * 64
+ *                         bytes, one process per GPU); the own entry is ignored. */
+int eik_slab_p2p_init(eik_plan* plan, int world, int rank, int64_t c0_local, int64_t ks, void** arena,
+                      int64_t* arena_bytes, void* ipc_handle);
+int eik_slab_p2p_connect(eik_plan* plan, void* const* peer_arenas, const void* ipc_handles);
 
 /* tau sweep (the kernel-reuse of R/experiments.py:74-109):
  * one plan caches exp(-|x|/tau_i) spectra for n_taus values; eik_run_sweep

@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 EIK_OK, EIK_EVALIDATION, EIK_EUNDERFLOW, EIK_ECUDA = 0, 1, 2, 3
 FIELD_PHI, FIELD_S, FIELD_GRAD, FIELD_HESS, FIELD_WINDING, FIELD_DEGREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
-HOST_INPUTS, HOST_OUTPUTS, SYNC, CHECK_UNDERFLOW, PROFILE = 0x1, 0x2, 0x4, 0x8, 0x10
+HOST_INPUTS, HOST_OUTPUTS, SYNC, CHECK_UNDERFLOW, PROFILE, SLAB_P2P = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 PASS_NAMES = ("prep", "col", "col_sign", "lines", "row")
 
 _i64p = C.POINTER(C.c_int64)
@@ -67,6 +67,9 @@ def lib():
             L.eik_pass_times.argtypes = [C.c_void_p, _f64p, C.c_int]
             L.eik_plan_create_slab.argtypes = [C.c_int, _i64p, C.c_double, C.c_double, C.c_uint32, C.c_int,
                                                C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]
+            L.eik_slab_p2p_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
+                                             C.c_void_p, C.c_void_p]
+            L.eik_slab_p2p_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
             L.eik_plan_create_sweep.argtypes = [C.c_int, _i64p, C.c_double, _f64p, C.c_int, C.c_int,
                                                 C.POINTER(C.c_void_p)]
             L.eik_run_sweep.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32,
@@ -84,7 +87,7 @@ def lib():
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
                          "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
                          "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep",
-                         "eik_classify"):
+                         "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect"):
                 getattr(L, name).restype = C.c_int
             _lib = L
         return _lib
@@ -93,7 +96,7 @@ def lib():
 def exported_symbols():
     return ["eik_plan_create", "eik_plan_create_slab", "eik_plan_destroy", "eik_plan_info", "eik_run",
             "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
-            "eik_plan_create_sweep", "eik_run_sweep", "eik_classify",
+            "eik_plan_create_sweep", "eik_run_sweep", "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect",
             "eik_last_error", "eik_version"]
 
 
@@ -145,25 +148,49 @@ class Plan:
         return {"padded": tuple(pad), "lines": lines.value, "device_bytes": nbytes.value}
 
     # -- slab-decomposed 3-D passes (device tensors; see include/eikfld_b200.h)
-    def slab_planes(self, group, nodes, weights, c0_local, ks, v_out, stream=None):
+    def slab_planes(self, group, nodes, weights, c0_local, ks, v_out=None, stream=None, p2p=False):
+        v_out = v_out or []
         arr = (C.c_void_p * 3)(*[_ptr(t) for t in v_out], *([None] * (3 - len(v_out))))
         check(lib().eik_slab_planes(self._h, int(group), _ptr(nodes), int(nodes.shape[0]),
-                                    _ptr(weights), int(c0_local), int(ks), arr, 0, stream))
+                                    _ptr(weights), int(c0_local), int(ks), arr, SLAB_P2P if p2p else 0, stream))
 
-    def slab_axis0(self, group, v_in, k1_begin, ks, w_out, stream=None):
+    def slab_axis0(self, group, v_in, k1_begin, ks, w_out, stream=None, p2p=False):
+        v_in, w_out = v_in or [], w_out or []
         vi = (C.c_void_p * 3)(*[_ptr(t) for t in v_in], *([None] * (3 - len(v_in))))
         wo = (C.c_void_p * 8)(*[_ptr(t) for t in w_out], *([None] * (8 - len(w_out))))
-        check(lib().eik_slab_axis0(self._h, int(group), vi, int(k1_begin), int(ks), wo, 0, stream))
+        check(lib().eik_slab_axis0(self._h, int(group), vi, int(k1_begin), int(ks), wo, SLAB_P2P if p2p else 0,
+                                   stream))
+
+    def slab_p2p_init(self, world, rank, c0_local, ks):
+        """Allocate the peer-to-peer exchange arena -> (device pointer, bytes, 64-byte IPC handle)."""
+        arena = C.c_void_p()
+        nbytes = C.c_int64()
+        handle = (C.c_char * 64)()
+        check(lib().eik_slab_p2p_init(self._h, int(world), int(rank), int(c0_local), int(ks), C.byref(arena),
+                                      C.byref(nbytes), handle))
+        return arena.value, nbytes.value, bytes(handle)
+
+    def slab_p2p_connect(self, peer_arenas=None, ipc_handles=None):
+        """Peers by device pointer (same process) or by IPC handle (list of 64-byte strings)."""
+        pa = None
+        if peer_arenas is not None:
+            pa = (C.c_void_p * len(peer_arenas))(*peer_arenas)
+        hb = None
+        if ipc_handles is not None:
+            hb = C.create_string_buffer(b"".join(ipc_handles), 64 * len(ipc_handles))
+        check(lib().eik_slab_p2p_connect(self._h, pa, hb))
 
     def slab_finish(self, w, c0_local, ks, *, S=None, grad=(None, None, None), mu=None, mask=None,
-                    underflow=None, d_count=None, stream=None):
+                    underflow=None, d_count=None, stream=None, p2p=False):
+        w = w or []
         wa = (C.c_void_p * 8)(*[_ptr(t) for t in w], *([None] * (8 - len(w))))
         out = Outputs()
         out.S, out.mu, out.mask, out.underflow = (_ptr(x) for x in (S, mu, mask, underflow))
         for d in range(3):
             out.grad[d] = _ptr(grad[d]) if d < len(grad) else None
         out.d_underflow_count = _ptr(d_count)
-        check(lib().eik_slab_finish(self._h, wa, int(c0_local), int(ks), C.byref(out), 0, stream))
+        check(lib().eik_slab_finish(self._h, wa, int(c0_local), int(ks), C.byref(out), SLAB_P2P if p2p else 0,
+                                    stream))
 
     def pass_times(self):
         """Device ms per pass of the last profiled run ({name: ms}, absent passes omitted)."""

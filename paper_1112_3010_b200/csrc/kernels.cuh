@@ -30,6 +30,7 @@
 namespace eik {
 
 constexpr int MAXC = 8;
+constexpr int MAXG = 8;  // ranks of a peer-to-peer slab exchange
 
 enum { IN_SPARSE = 0, IN_DENSE = 1 };
 enum { OUT_COMPS = 0, OUT_SUM = 1, OUT_SPECTRUM = 2 };
@@ -189,7 +190,22 @@ struct ColArgs {
   int64_t spec_ld;
   const double2* tw;
   int lmax;
+  // Peer-block outputs (slab exchange fused into the pass, P2P over NVLink):
+  // when blk[0] is set, output row n of component j is written to
+  // blk[n >> blk_shift] + j * blk_cstride + item * out_item + (n mod 2^blk_shift) * out_es + l,
+  // i.e. straight into the receive buffer of the rank that owns row n.
+  double2* blk[MAXG];
+  int blk_shift;
+  int64_t blk_cstride;
 };
+
+// Destination of output row n of component j (own buffer or a peer's block).
+__device__ __forceinline__ double2* comp_dst(const ColArgs& a, int j, int64_t item, int64_t l, int n) {
+  if (a.blk[0])
+    return a.blk[n >> a.blk_shift] + j * a.blk_cstride + item * a.out_item +
+           (int64_t)(n & ((1 << a.blk_shift) - 1)) * a.out_es + l;
+  return a.out[j] + item * a.out_item + (int64_t)n * a.out_es + l;
+}
 
 __device__ __forceinline__ double2 kmul(double2 x, const KSpec& k, int64_t l, int k0, int M0) {
   if (k.cplx) return cmul(x, __ldg(k.cplx + (int64_t)k0 * k.ld + l));
@@ -322,12 +338,11 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
         for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kmul(v[r], a.ks[j], l, LN::out_idx(t, r), LN::M) : v[r];
       }
       fft_line<LN, true>(y, t, xb, tws);
-      double2* dst = a.out[j] + item * a.out_item + l;
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
         if (LN::L > 0 && LN::upper_in(r)) continue;
         const int n = LN::in_idx(t, r);
-        if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = y[r];
+        if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = y[r];
       }
     }
   } else if constexpr (OUT == OUT_SUM) {
@@ -352,12 +367,11 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       }
     }
     fft_line<LN, true>(y, t, xb, tws);
-    double2* dst = a.out[0] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
       if (LN::L > 0 && LN::upper_in(r)) continue;
       const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = y[r];
+      if (valid && n < a.n_out) *comp_dst(a, 0, item, l, n) = y[r];
     }
   } else {  // OUT_SPECTRUM
 #pragma unroll 1
@@ -475,12 +489,11 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       if (i + 1 < a.n_in) tmem_put(ta, v);
     }
     fft_line<LN, true>(v, t, xb, tws);
-    double2* dst = a.out[0] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
       if (LN::L > 0 && LN::upper_in(r)) continue;
       const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = v[r];
+      if (valid && n < a.n_out) *comp_dst(a, 0, item, l, n) = v[r];
     }
     tmem_free_cta(tbase, TC::COLS);
     return;
@@ -504,12 +517,11 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       }
     }
     fft_line<LN, true>(v, t, xb, tws);
-    double2* dst = a.out[j] + item * a.out_item + l;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
       if (LN::L > 0 && LN::upper_in(r)) continue;
       const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out) dst[(int64_t)n * a.out_es] = v[r];
+      if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = v[r];
     }
   }
   tmem_free_cta(tbase, TC::COLS);
@@ -551,6 +563,10 @@ struct LinesArgs {
   double scale;
   const double2* tw;
   int lmax;
+  // peer-block outputs (see ColArgs::blk): element n of component c goes to
+  // blk[n >> split_shift_out] + c * blk_cstride + o * outer_out + q + (n mod 2^shift) * es_out
+  double2* blk[MAXG];
+  int64_t blk_cstride;
 };
 
 template <int L, bool INV, bool HALF>
@@ -591,8 +607,9 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
     if (n < a.n_out) {
       double2 x = v[r];
       if (a.scale != 1.0) { x.x *= a.scale; x.y *= a.scale; }
-      dst[(int64_t)(n >> a.split_shift_out) * a.split_stride_out +
-          (int64_t)(n & ((1 << a.split_shift_out) - 1)) * a.es_out] = x;
+      const int64_t in_blk = (int64_t)(n & ((1 << a.split_shift_out) - 1)) * a.es_out;
+      if (a.blk[0]) a.blk[n >> a.split_shift_out][c * a.blk_cstride + o * a.outer_out + q + in_blk] = x;
+      else dst[(int64_t)(n >> a.split_shift_out) * a.split_stride_out + in_blk] = x;
     }
   }
 }

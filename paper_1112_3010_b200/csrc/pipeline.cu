@@ -129,7 +129,15 @@ struct eik_plan {
   cudaStream_t st2 = nullptr, st_copy = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr;
   DevBuf serr, trows, tsign;
+  // peer-to-peer slab exchange: own arena [P2P_NV V slots][n_comp W slots]
+  // and every rank's arena base (own, same-process or IPC-opened)
+  DevBuf p2p;
+  int p2p_world = 0, p2p_rank = 0;
+  int64_t p2p_c0loc = 0, p2p_ks = 0, p2p_slot = 0;  // complex elements per slot
+  std::vector<double2*> p2p_peer;
+  std::vector<void*> p2p_opened;
   ~eik_plan() {
+    for (void* q : p2p_opened) cudaIpcCloseMemHandle(q);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -143,7 +151,7 @@ struct eik_plan {
     return D == 2 ? (int64_t)c[0] * H : (int64_t)c[0] * M[1] * H;
   }
   int64_t held() const {
-    int64_t b = tw.bytes + comp.bytes + vin.bytes + trows.bytes + tsign.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
+    int64_t b = p2p.bytes + tw.bytes + comp.bytes + vin.bytes + trows.bytes + tsign.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
                 scols.bytes + srowptr.bytes + stage.bytes + work.bytes + h_nodes.bytes + h_off.bytes +
                 h_snodes.bytes + h_sw.bytes;
     for (auto& k : kdist) b += k->buf.bytes;
@@ -551,8 +559,15 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
 // 3-D pass A: impulse DFT along axis 2 + FFT along axis 1 for planes [0, c0loc)
 // of the (slab-relative) node list.  V[i] rows k1 are packed by k1-slab:
 // [k1 / ks][i0][k1 % ks][k2] (ks = M1: plain [i0][k1][k2]).
+// Peer-block destinations of a pass whose output is exchanged (see ColArgs::blk).
+struct PeerBlk {
+  double2* blk[MAXG] = {};
+  int shift = 0;
+  int64_t cstride = 0;
+};
+
 int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
-                int64_t c0loc, int64_t ks, double2* const* V, cudaStream_t st) {
+                int64_t c0loc, int64_t ks, double2* const* V, cudaStream_t st, const PeerBlk* pb = nullptr) {
   const int64_t H = p->H, c1 = p->c[1], c2 = p->c[2];
   DevBuf& rid = sg ? p->srowid : p->rowid;
   DevBuf& cl = sg ? p->scols : p->cols;
@@ -598,8 +613,13 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
     }
     la.n_valid = (int)c1;
     la.n_out = p->M[1];
+    if (pb) {
+      for (int g = 0; g < MAXG; ++g) la.blk[g] = pb->blk[g];
+      la.blk_cstride = pb->cstride;
+    }
     return launch_lines<false, true>(p->L[1], la, n_in, st);
   }
+  if (pb) return fail(EIK_EVALIDATION, "the peer-to-peer slab exchange needs the row-DFT planes pass");
   ColArgs a = col_defaults(p);
   a.rowptr = rp.as<int64_t>();
   a.cols = cl.as<int32_t>();
@@ -624,7 +644,7 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
 // 3-D pass B: fused axis-0 pass for k1 in [k1b, k1b + ks) over spectra
 // V[i][i0 < c0][k1'][k2]; writes W_j[n < c0][k1'][k2].
 int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks, int64_t B, const Roles& r,
-               double2* const* W, cudaStream_t st) {
+               double2* const* W, cudaStream_t st, const PeerBlk* pb = nullptr) {
   const int64_t H = p->H;
   if (k1b * H < p->ks_l0 || (k1b + ks) * H > p->ks_l0 + p->ks_lines)
     return fail(EIK_EVALIDATION, "k1 slab not covered by the plan's kernel spectra");
@@ -639,6 +659,11 @@ int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks,
   a.out_es = ks * H;
   a.out_item = (int64_t)p->c[0] * ks * H;
   set_components(p, sg, r, a, W, k1b * H);
+  if (pb) {
+    for (int g = 0; g < MAXG; ++g) a.blk[g] = pb->blk[g];
+    a.blk_shift = pb->shift;
+    a.blk_cstride = pb->cstride;
+  }
   return sg ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st)
             : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st);
 }
@@ -974,14 +999,93 @@ static int slab_roles(const eik_plan* p, Roles& r) {
   return EIK_OK;
 }
 
-int eik_slab_planes(eik_plan* p, int group, const int64_t* nodes, int64_t n_nodes, const double* weights,
-                    int64_t c0_local, int64_t ks, double* const* v_out, uint32_t flags, void* stream) {
-  if (!p || !v_out) return fail(EIK_EVALIDATION, "null argument");
+// Peer-to-peer slab arena: V slots (group 0: delta_Y -> slot 0; group 1: the
+// three flux fields -> slots 1..3), then one W slot per component.
+constexpr int P2P_NV = 4;
+static int64_t p2p_vslot(int group) { return group ? 1 : 0; }
+static int64_t p2p_block(const eik_plan* p) { return p->p2p_c0loc * p->p2p_ks * p->H; }
+static int p2p_check(const eik_plan* p, int64_t c0_local, int64_t ks) {
+  if (!p->p2p.p || (int)p->p2p_peer.size() != p->p2p_world)
+    return fail(EIK_EVALIDATION, "peer-to-peer slab exchange not initialised / connected");
+  for (auto* q : p->p2p_peer)
+    if (!q) return fail(EIK_EVALIDATION, "peer-to-peer slab exchange not connected");
+  if (c0_local != p->p2p_c0loc || ks != p->p2p_ks) return fail(EIK_EVALIDATION, "slab geometry differs from p2p_init");
+  return EIK_OK;
+}
+
+int eik_slab_p2p_init(eik_plan* p, int world, int rank, int64_t c0_local, int64_t ks, void** arena,
+                      int64_t* arena_bytes, void* ipc_handle) {
+  if (!p) return fail(EIK_EVALIDATION, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   CK(cudaSetDevice(p->device));
   Roles r;
   int rc = slab_roles(p, r);
   if (rc) return rc;
+  if (world < 1 || world > MAXG || rank < 0 || rank >= world)
+    return fail(EIK_EVALIDATION, "peer-to-peer slab exchange supports 1..8 ranks");
+  if (c0_local < 1 || (c0_local & (c0_local - 1)) || c0_local * world != p->c[0] || ks * world != p->M[1])
+    return fail(EIK_EVALIDATION, "bad slab geometry (c0/G must be a power of two, M1 = G * ks)");
+  p->p2p_world = world;
+  p->p2p_rank = rank;
+  p->p2p_c0loc = c0_local;
+  p->p2p_ks = ks;
+  p->p2p_slot = (int64_t)world * c0_local * ks * p->H;
+  const size_t bytes = (size_t)(P2P_NV + r.n_comp()) * p->p2p_slot * sizeof(double2);
+  CK(p->p2p.ensure(bytes));
+  for (void* q : p->p2p_opened) cudaIpcCloseMemHandle(q);
+  p->p2p_opened.clear();
+  p->p2p_peer.assign(world, nullptr);
+  p->p2p_peer[rank] = p->p2p.as<double2>();
+  if (arena) *arena = p->p2p.p;
+  if (arena_bytes) *arena_bytes = (int64_t)bytes;
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, p->p2p.p));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+  }
+  return EIK_OK;
+}
+
+int eik_slab_p2p_connect(eik_plan* p, void* const* peer_arenas, const void* ipc_handles) {
+  if (!p || (!peer_arenas && !ipc_handles)) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  if (!p->p2p.p) return fail(EIK_EVALIDATION, "eik_slab_p2p_init first");
+  for (int g = 0; g < p->p2p_world; ++g) {
+    if (g == p->p2p_rank) continue;
+    if (peer_arenas && peer_arenas[g]) {
+      p->p2p_peer[g] = static_cast<double2*>(peer_arenas[g]);
+    } else if (ipc_handles) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(ipc_handles) + (size_t)g * sizeof(h), sizeof(h));
+      void* q = nullptr;
+      CK(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+      p->p2p_opened.push_back(q);
+      p->p2p_peer[g] = static_cast<double2*>(q);
+    } else {
+      return fail(EIK_EVALIDATION, "no arena or IPC handle for a peer rank");
+    }
+  }
+  return EIK_OK;
+}
+
+int eik_slab_planes(eik_plan* p, int group, const int64_t* nodes, int64_t n_nodes, const double* weights,
+                    int64_t c0_local, int64_t ks, double* const* v_out, uint32_t flags, void* stream) {
+  const bool p2p = flags & EIK_SLAB_P2P;
+  if (!p || (!v_out && !p2p)) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  Roles r;
+  int rc = slab_roles(p, r);
+  if (rc) return rc;
+  PeerBlk pb;
+  if (p2p) {
+    if ((rc = p2p_check(p, c0_local, ks))) return rc;
+    // this rank's block of every destination's V slots
+    for (int g = 0; g < p->p2p_world; ++g)
+      pb.blk[g] = p->p2p_peer[g] + p2p_vslot(group) * p->p2p_slot + p->p2p_rank * p2p_block(p);
+    pb.cstride = p->p2p_slot;
+  }
   if (group == 1 && !r.sign) return fail(EIK_EVALIDATION, "plan was built without sign kernels");
   if (group == 0 && !r.phi) return fail(EIK_EVALIDATION, "plan was built without the distance kernels");
   if (ks < 1 || p->M[1] % ks || (ks & (ks - 1)) || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
@@ -990,15 +1094,22 @@ int eik_slab_planes(eik_plan* p, int group, const int64_t* nodes, int64_t n_node
   CK(off.ensure(2 * sizeof(int64_t)));
   const int64_t o[2] = {0, n_nodes};
   CK(cudaMemcpyAsync(off.p, o, sizeof(o), cudaMemcpyHostToDevice, st));
-  double2* V[3] = {(double2*)v_out[0], group ? (double2*)v_out[1] : nullptr, group ? (double2*)v_out[2] : nullptr};
-  if ((rc = pass_planes(p, group == 1, nodes, off.as<int64_t>(), n_nodes, 1, weights, c0_local, ks, V, st))) return rc;
+  double2* V[3] = {nullptr, nullptr, nullptr};
+  if (!p2p) {
+    V[0] = (double2*)v_out[0];
+    if (group) { V[1] = (double2*)v_out[1]; V[2] = (double2*)v_out[2]; }
+  }
+  if ((rc = pass_planes(p, group == 1, nodes, off.as<int64_t>(), n_nodes, 1, weights, c0_local, ks, V, st,
+                        p2p ? &pb : nullptr)))
+    return rc;
   if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
   return EIK_OK;
 }
 
 int eik_slab_axis0(eik_plan* p, int group, double* const* v_in, int64_t k1_begin, int64_t ks, double* const* w_out,
                    uint32_t flags, void* stream) {
-  if (!p || !v_in || !w_out) return fail(EIK_EVALIDATION, "null argument");
+  const bool p2p = flags & EIK_SLAB_P2P;
+  if (!p || (!p2p && (!v_in || !w_out))) return fail(EIK_EVALIDATION, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   CK(cudaSetDevice(p->device));
   Roles r;
@@ -1006,28 +1117,47 @@ int eik_slab_axis0(eik_plan* p, int group, double* const* v_in, int64_t k1_begin
   if (rc) return rc;
   if (ks < 1 || p->M[1] % ks || k1_begin < 0 || k1_begin + ks > p->M[1]) return fail(EIK_EVALIDATION, "bad slab geometry");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double2* V[3] = {(double2*)v_in[0], group ? (double2*)v_in[1] : nullptr, group ? (double2*)v_in[2] : nullptr};
+  double2* V[3] = {nullptr, nullptr, nullptr};
   std::vector<double2*> W(r.n_comp(), nullptr);
-  if (group) W[r.n_dist()] = (double2*)w_out[0];
-  else
-    for (int j = 0; j < r.n_dist(); ++j) W[j] = (double2*)w_out[j];
-  if ((rc = pass_axis0(p, group == 1, V, k1_begin, ks, 1, r, W.data(), st))) return rc;
+  PeerBlk pb;
+  if (p2p) {
+    if ((rc = p2p_check(p, p->c[0] / (p->p2p_world ? p->p2p_world : 1), ks))) return rc;
+    if (k1_begin != p->p2p_rank * ks) return fail(EIK_EVALIDATION, "k1 slab does not match the rank");
+    double2* own = p->p2p_peer[p->p2p_rank];
+    for (int i = 0; i < (group ? 3 : 1); ++i) V[i] = own + (p2p_vslot(group) + i) * p->p2p_slot;
+    // rows of every owner's W slots; component j at + j * slot (the sign sum is slot n_dist)
+    const int j0 = group ? r.n_dist() : 0;
+    for (int g = 0; g < p->p2p_world; ++g)
+      pb.blk[g] = p->p2p_peer[g] + (P2P_NV + j0) * p->p2p_slot + p->p2p_rank * p2p_block(p);
+    pb.shift = ilog2_exact(p->p2p_c0loc);
+    pb.cstride = p->p2p_slot;
+  } else {
+    V[0] = (double2*)v_in[0];
+    if (group) { V[1] = (double2*)v_in[1]; V[2] = (double2*)v_in[2]; }
+    if (group) W[r.n_dist()] = (double2*)w_out[0];
+    else
+      for (int j = 0; j < r.n_dist(); ++j) W[j] = (double2*)w_out[j];
+  }
+  if ((rc = pass_axis0(p, group == 1, V, k1_begin, ks, 1, r, W.data(), st, p2p ? &pb : nullptr))) return rc;
   if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
   return EIK_OK;
 }
 
 int eik_slab_finish(eik_plan* p, double* const* w, int64_t c0_local, int64_t ks, const eik_outputs* out,
                     uint32_t flags, void* stream) {
-  if (!p || !w || !out) return fail(EIK_EVALIDATION, "null argument");
+  const bool p2p = flags & EIK_SLAB_P2P;
+  if (!p || (!w && !p2p) || !out) return fail(EIK_EVALIDATION, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   CK(cudaSetDevice(p->device));
   Roles r;
   int rc = slab_roles(p, r);
   if (rc) return rc;
   if (ks < 1 || p->M[1] % ks || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
+  if (p2p && (rc = p2p_check(p, c0_local, ks))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   std::vector<double2*> W(r.n_comp());
-  for (int j = 0; j < r.n_comp(); ++j) W[j] = (double2*)w[j];
+  for (int j = 0; j < r.n_comp(); ++j)
+    W[j] = p2p ? p->p2p_peer[p->p2p_rank] + (P2P_NV + j) * p->p2p_slot : (double2*)w[j];
   RowArgs ra{};
   ra.S = out->S;
   for (int d = 0; d < 3; ++d) ra.grad[d] = out->grad[d];

@@ -23,6 +23,13 @@ the same kernel the single-GPU path runs (`eik_run` on a 3-D plan is this
 schedule with G = 1), so a G-rank result is bit-identical to the one-GPU
 result.  Each rank's plan caches only its k1-slab of the kernel spectra.
 
+The fused variant (`run_rank_p2p`, `CudaSlabExecutor(p2p=True)`) removes the
+all-to-alls: the planes and axis-0 kernels store their output blocks straight
+into the owning rank's receive arena through CUDA-IPC peer pointers (NVLink /
+NVSwitch stores, overlapped with the transforms), leaving two stream-ordered
+barriers per step.  It is bit-identical to the NCCL schedule (same kernels,
+same arithmetic; only the store addresses differ).
+
 `run_rank` is written against an executor interface (planes / axis0 /
 finish plus the V/W buffers) and an `exchange(send, recv)` callable, so the
 same orchestration runs with the CUDA executor over NCCL, with several CUDA
@@ -100,6 +107,66 @@ def nccl_exchange(dist):
     return exchange
 
 
+def run_rank_p2p(ex, barrier, nodes, sign_nodes=None, sign_weights=None):
+    """One rank of the fused peer-to-peer schedule (EIK_SLAB_P2P).
+
+    The planes passes store their k1-slab blocks straight into the owners' V
+    slots and the axis-0 passes store their rows straight into the owners' W
+    slots (NVLink stores through peer pointers, overlapped with the transforms),
+    so the only cross-rank operations are two stream-ordered barriers: after
+    the planes passes (every V block landed) and after the axis-0 passes (every
+    W block landed).  The distance and sign groups use disjoint slots, so their
+    planes passes and their axis-0 passes run back to back.
+    """
+    ex.planes(0, nodes, None)
+    sign = ex.sign and sign_nodes is not None
+    if sign:
+        ex.planes(1, sign_nodes, sign_weights)
+    barrier()
+    ex.axis0(0)
+    if sign:
+        ex.axis0(1)
+    barrier()
+    return ex.finish()
+
+
+def stream_barrier(dist, device):
+    """Cross-rank barrier ordered on the current stream (one 8-byte all-reduce)."""
+    import torch
+
+    flag = torch.zeros(1, dtype=torch.float64, device=device)
+
+    def barrier():
+        dist.all_reduce(flag)
+
+    return barrier
+
+
+def connect_p2p(ex, dist):
+    """Exchange the arenas' CUDA IPC handles (one process per GPU) and open the peers."""
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, ex.ipc_handle)
+    ex.plan.slab_p2p_connect(ipc_handles=handles)
+
+
+def run_emulated_p2p(executors, node_lists):
+    """All ranks of the peer-to-peer schedule in one process (peer arenas by
+    device pointer), phase by phase: no rank ever waits on another."""
+    arenas = [ex.arena for ex in executors]
+    for ex in executors:
+        ex.plan.slab_p2p_connect(peer_arenas=arenas)
+    sign = executors[0].sign and node_lists[0][1] is not None
+    for r, ex in enumerate(executors):
+        ex.planes(0, node_lists[r][0], None)
+        if sign:
+            ex.planes(1, node_lists[r][1], node_lists[r][2])
+    for ex in executors:
+        ex.axis0(0)
+        if sign:
+            ex.axis0(1)
+    return [ex.finish() for ex in executors]
+
+
 def run_emulated(executors, node_lists):
     """All ranks in one process: phase by phase, exchanges as block copies.
 
@@ -133,7 +200,7 @@ def run_emulated(executors, node_lists):
 class CudaSlabExecutor:
     """CUDA passes of one rank (libeikfld_b200 slab API) with torch device buffers."""
 
-    def __init__(self, grid, tau, world, rank, *, grad=True, sign=True, device=0):
+    def __init__(self, grid, tau, world, rank, *, grad=True, sign=True, device=0, p2p=False):
         import torch
 
         from . import _native
@@ -156,6 +223,14 @@ class CudaSlabExecutor:
         n_in = 3 if sign else 1
         self.n_dist = 1 + (3 if grad else 0)
         n_comp = self.n_dist + (1 if sign else 0)
+        self.p2p = p2p
+        self.N_local = L.c0loc * L.plane_nodes
+        if p2p:
+            # one arena per rank in the receive layout; the passes store into the
+            # owners' arenas, so no send / staging buffers exist at all
+            self.arena, self.arena_bytes, self.ipc_handle = self.plan.slab_p2p_init(L.world, L.rank, L.c0loc, L.ks)
+            self.V_send = self.V_recv = self.W = self.W_recv = None
+            return
         self.V_send = [mk() for _ in range(n_in)]
         self.V_recv = [mk() for _ in range(n_in)]
         self.W = [mk() for _ in range(n_comp)]
@@ -184,10 +259,16 @@ class CudaSlabExecutor:
         nd = dev(nodes, np.int64)
         wt = dev(weights, np.float64)
         self._keep = (nd, wt)
-        self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, self.V_send[:3 if group else 1], self._stream())
+        if self.p2p:
+            self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, None, self._stream(), p2p=True)
+        else:
+            self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, self.V_send[:3 if group else 1], self._stream())
 
     def axis0(self, group):
         L = self.layout
+        if self.p2p:
+            self.plan.slab_axis0(group, None, L.k1_begin, L.ks, None, self._stream(), p2p=True)
+            return
         out = [self.W[self.n_dist]] if group else self.W[: self.n_dist]
         self.plan.slab_axis0(group, self.V_recv[:3 if group else 1], L.k1_begin, L.ks, out, self._stream())
 
@@ -204,5 +285,5 @@ class CudaSlabExecutor:
             out["mask"] = torch.empty(self.N_local, dtype=torch.uint8, device=self.dev)
         self.plan.slab_finish(self.W_recv, L.c0loc, L.ks, S=out["S"], grad=out.get("grad", (None,) * 3),
                               mu=out.get("mu"), mask=out.get("mask"), underflow=out["underflow"],
-                              stream=self._stream())
+                              stream=self._stream(), p2p=self.p2p)
         return out

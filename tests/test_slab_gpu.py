@@ -1,5 +1,7 @@
 """GPU: the slab-decomposed 3-D schedule (ranks emulated in one process, no
-cross-rank waiting) reproduces the single-GPU pipeline bit for bit."""
+cross-rank waiting) reproduces the single-GPU pipeline bit for bit, both with
+the NCCL-style exchange (block copies) and with the exchange fused into the
+passes (peer-pointer stores into the owners' arenas, EIK_SLAB_P2P)."""
 
 import numpy as np
 import pytest
@@ -7,12 +9,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("world", [1, 2, 4])
-def test_emulated_slab_bit_identical(cuda_ok, world):
+def test_emulated_slab_bit_identical(cuda_ok, world, p2p):
     import torch
 
     from paper_1112_3010_b200 import GridSpec, engine, workloads
-    from paper_1112_3010_b200.slab import CudaSlabExecutor, local_nodes, run_emulated
+    from paper_1112_3010_b200.slab import CudaSlabExecutor, local_nodes, run_emulated, run_emulated_p2p
 
     grid = GridSpec((-15.5, -15.5, -15.5), 1.0, (32, 32, 32))
     tau = 0.75
@@ -24,13 +27,13 @@ def test_emulated_slab_bit_identical(cuda_ok, world):
     sn, sw = dt.sign_inputs(surf)
     ref = dt.run_host(nodes, sign_nodes=sn, sign_weights=sw)
 
-    exs = [CudaSlabExecutor(grid, tau, world, r) for r in range(world)]
+    exs = [CudaSlabExecutor(grid, tau, world, r, p2p=p2p) for r in range(world)]
     lists = []
     for ex in exs:
         ln, _ = local_nodes(nodes, ex.layout)
         lsn, lsw = local_nodes(sn, ex.layout, sw)
         lists.append((ln, lsn, lsw))
-    outs = run_emulated(exs, lists)
+    outs = (run_emulated_p2p if p2p else run_emulated)(exs, lists)
     torch.cuda.synchronize()
     got = {k: torch.cat([o[k] for o in outs]).cpu().numpy() for k in ("S", "mu", "mask")}
     for a in range(3):
@@ -40,3 +43,25 @@ def test_emulated_slab_bit_identical(cuda_ok, world):
     assert np.array_equal(got["mask"], ref["mask"])
     for a in range(3):
         assert np.array_equal(got[f"g{a}"], ref["grad"][a], equal_nan=True)
+
+
+def test_p2p_slab_repeat_and_validation(cuda_ok):
+    """Two consecutive steps through the same arenas agree; geometry is checked."""
+    import torch
+
+    from paper_1112_3010_b200 import GridSpec, ValidationError
+    from paper_1112_3010_b200._native import NativeError
+    from paper_1112_3010_b200.slab import CudaSlabExecutor, local_nodes, run_emulated_p2p
+
+    grid = GridSpec((0.0, 0.0, 0.0), 1.0, (16, 12, 10))
+    rng = np.random.Generator(np.random.PCG64(9))
+    nodes = np.sort(rng.choice(grid.num_nodes, 60, replace=False))
+    exs = [CudaSlabExecutor(grid, 1.0, 2, r, sign=False, p2p=True) for r in range(2)]
+    lists = [(local_nodes(nodes, ex.layout)[0], None, None) for ex in exs]
+    a = run_emulated_p2p(exs, lists)
+    b = run_emulated_p2p(exs, lists)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.equal(x["S"], y["S"])
+    with pytest.raises((ValidationError, NativeError)):
+        exs[0].plan.slab_finish(None, 3, exs[0].layout.ks, S=a[0]["S"], p2p=True)
