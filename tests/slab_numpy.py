@@ -89,3 +89,67 @@ class NumpySlabExecutor:
         if self.sign:
             out["mu"] = -comps[-1] / (4.0 * math.pi)
         return out
+
+
+class NumpyP2PSlabExecutor(NumpySlabExecutor):
+    """The fused peer-to-peer schedule on CPU ranks: every rank's receive arena
+    is a shared-memory segment laid out like the CUDA arena ([4 V slots][W
+    slots] of [G src][c0/G][ks][H2] complex); planes / axis0 store their blocks
+    straight into the owners' arenas, finish reads its own.  The only
+    cross-rank operations are the two barriers of slab.run_rank_p2p."""
+
+    NV = 4
+
+    def __init__(self, *args, **kw):
+        from multiprocessing import shared_memory
+
+        super().__init__(*args, **kw)
+        L = self.layout
+        self.n_slots = self.NV + len(self.W)
+        self.slot = L.world * L.block
+        self.shm = shared_memory.SharedMemory(create=True, size=self.n_slots * self.slot * 16)
+        self.name = self.shm.name
+        self.peers = None
+
+    def _arena(self, shm):
+        L = self.layout
+        return np.ndarray((self.n_slots, L.world, L.block), dtype=np.complex128, buffer=shm.buf)
+
+    def connect(self, names):
+        from multiprocessing import shared_memory
+
+        self._opened = [self.shm if n == self.name else shared_memory.SharedMemory(name=n) for n in names]
+        self.peers = [self._arena(s) for s in self._opened]
+
+    def planes(self, group, nodes, weights):
+        super().planes(group, nodes, weights)  # fills V_send[i][dest]
+        L = self.layout
+        base = 1 if group else 0
+        for i in range(3 if group else 1):
+            for dest in range(L.world):
+                self.peers[dest][base + i, L.rank] = self.V_send[i][dest]
+
+    def axis0(self, group):
+        L = self.layout
+        own = self.peers[L.rank]
+        base = 1 if group else 0
+        for i in range(3 if group else 1):
+            self.V_recv[i][:] = own[base + i]
+        super().axis0(group)  # fills W[j][dest]
+        js = [self.n_dist] if group else range(self.n_dist)
+        for j in js:
+            for dest in range(L.world):
+                self.peers[dest][self.NV + j, L.rank] = self.W[j][dest]
+
+    def finish(self):
+        own = self.peers[self.layout.rank]
+        for j in range(len(self.W_recv)):
+            self.W_recv[j][:] = own[self.NV + j]
+        return super().finish()
+
+    def close(self):
+        for s in self._opened:
+            if s is not self.shm:
+                s.close()
+        self.shm.close()
+        self.shm.unlink()

@@ -36,20 +36,32 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, p2p=False):
     import torch
     import torch.distributed as dist
 
-    from paper_1112_3010_b200.slab import local_nodes, run_rank
-    from slab_numpy import NumpySlabExecutor
+    from paper_1112_3010_b200.slab import local_nodes, run_rank, run_rank_p2p
+    from slab_numpy import NumpyP2PSlabExecutor, NumpySlabExecutor
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ex = NumpySlabExecutor(COUNTS, H_SP, TAU, world, rank)
+    ex = (NumpyP2PSlabExecutor if p2p else NumpySlabExecutor)(COUNTS, H_SP, TAU, world, rank)
     nodes, snodes, sw = _inputs()
     ln, _ = local_nodes(nodes, ex.layout)
     lsn, lsw = local_nodes(snodes, ex.layout, sw)
+    if p2p:
+        names = [None] * world
+        dist.all_gather_object(names, ex.name)
+        ex.connect(names)
+        dist.barrier()
+        out = run_rank_p2p(ex, dist.barrier, ln, lsn, lsw)
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), S=out["S"], phi=out["phi"], mu=out["mu"],
+                 gx=out["grad"][0], gy=out["grad"][1], gz=out["grad"][2])
+        dist.barrier()  # every peer is done with this rank's arena
+        ex.close()
+        dist.destroy_process_group()
+        return
 
     def exchange(send, recv):
         for s, r in zip(send, recv):
@@ -62,10 +74,12 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("world", [2])
-def test_slab_schedule_world2_gloo(world):
+def test_slab_schedule_world2_gloo(world, p2p):
+    """NCCL-style all-to-all schedule and the fused peer-store schedule."""
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), d, p2p), nprocs=world, join=True)
         parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
         got = {k: np.concatenate([p[k] for p in parts]) for k in ("S", "phi", "mu", "gx", "gy", "gz")}
     nodes, snodes, sw = _inputs()
