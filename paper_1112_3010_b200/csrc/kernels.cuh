@@ -236,6 +236,27 @@ __device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpe
     for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(k, l, LN::out_idx(t, r), LN::M);
   }
 }
+// L1 prefetch of this thread's EPT kernel-spectrum values (TMEM column kernel).
+#ifndef EIK_KPF
+#define EIK_KPF 1
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+template <class CFG>
+__device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t) {
+  using LN = typename CFG::LN;
+  if (k.perm) {
+    const double* src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NT + threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) prefetch_l1(src + r * CFG::NT);
+  } else {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) {
+      const int k0 = LN::out_idx(t, r);
+      const bool hi = k0 > (LN::M >> 1);
+      prefetch_l1(k.re + (int64_t)(hi ? LN::M - k0 : k0) * k.ld + l);
+    }
+  }
+}
 __device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0) {
   if (k.odd0 && k0 > (M0 >> 1)) v = -v;
   return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
@@ -502,6 +523,21 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
   fft_line<LN, false, HALF>(v, t, xb, tws);
   tmem_put(ta, v);
+#if EIK_KPF
+  // kernel spectra: the next component's lines are prefetched into L1 one
+  // transform ahead (no registers held across the FFT); loaded at use
+  if (valid) kprefetch_all<TC>(a.ks[0], l, t);
+#pragma unroll 1
+  for (int j = 0; j < a.n_comp; ++j) {
+    tmem_get(ta, v);
+    if (valid) {
+      double kn[LN::EPT];
+      kload_all<TC>(kn, a.ks[j], l, t);
+      if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], l, t);
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) v[r] = kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M);
+    }
+#else
   double kn[LN::EPT];
   if (valid) {
     kload_all<TC>(kn, a.ks[0], l, t);
@@ -516,6 +552,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
         kload_all<TC>(kn, a.ks[j + 1], l, t);
       }
     }
+#endif
     fft_line<LN, true>(v, t, xb, tws);
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {

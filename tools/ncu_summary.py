@@ -1,5 +1,6 @@
 """Summarise an ncu report: key metrics per kernel + top stall reasons."""
 import csv
+import re
 import subprocess
 import sys
 
@@ -30,11 +31,14 @@ for r in rr[2:]:
     name = r[h.index("Kernel Name")][:50]
     stalls = []
     for j, col in enumerate(h):
-        if col.startswith("smsp__average_warp_latency_issue_stalled_") and col.endswith(".ratio"):
+        m = re.fullmatch(r"smsp__pcsamp_warps_issue_stalled_([a-z_]+)", col)
+        if m and not m.group(1).endswith("not_issued"):
             try:
-                stalls.append((float(r[j]), col.replace("smsp__average_warp_latency_issue_stalled_", "")))
+                stalls.append((float(r[j]), m.group(1)))
             except ValueError:
                 pass
+    tot = sum(v for v, _ in stalls) or 1.0
+    stalls = [(100.0 * v / tot, n) for v, n in stalls]
     stalls.sort(reverse=True)
     extra = []
     for key in ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
@@ -43,5 +47,5 @@ for r in rr[2:]:
                 "sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "sm__sass_thread_inst_executed_op_dmul_pred_on.sum"):
         if key in h:
             extra.append(f"{key.split('.')[0]}={r[h.index(key)]}")
-    print(name, "stalls:", ", ".join(f"{n}={v:.1f}" for v, n in stalls[:6]))
+    print(name, "stall samples %:", ", ".join(f"{n}={v:.1f}" for v, n in stalls[:7]))
     print("   ", "; ".join(extra))

@@ -1,5 +1,6 @@
 # Round profile capture under gpurun (one GPU): launch lists of the bench
-# command (C2 default, C3, C5) and one ncu --set full capture of the C2 step.
+# command (C2 default, C3, C5) and one ncu --set full capture per config of
+# one device-resident step (tools/prof_step.py; plan-time kernels excluded).
 set -x
 OUT=gpurun_out/prof
 mkdir -p $OUT
@@ -7,8 +8,9 @@ for c in C2 C3 C5; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch_$c.log 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:col_tmem_kernel|row_kernel<|impulse_rows|lines_kernel' \
-  -c 5 -o $OUT/c2_full -f python tools/prof_step.py C2 1 > $OUT/ncu_full_c2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:col_tmem_kernel|row_kernel<|lines_kernel' \
-  -c 4 -o $OUT/c3_full -f python tools/prof_step.py C3 1 > $OUT/ncu_full_c3.log 2>&1
+K='regex:col_tmem_kernel|row_kernel|impulse_rows|lines_kernel'
+timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 5 -o $OUT/c2_full -f \
+  python tools/prof_step.py C2 1 > $OUT/ncu_full_c2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 6 -o $OUT/c3_full -f \
+  python tools/prof_step.py C3 1 > $OUT/ncu_full_c3.log 2>&1
 ls -la $OUT
