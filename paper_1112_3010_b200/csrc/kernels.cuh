@@ -491,13 +491,21 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     // y = sum_i K_i X_i accumulated in TMEM while each input is transformed in registers
 #pragma unroll 1
     for (int i = 0; i < a.n_in; ++i) {
+#if EIK_KPF
+      if (valid) kprefetch_all<TC>(a.ks[i], l, t);  // into L1 while the input is transformed
+#else
       double kn[LN::EPT];
       if (valid) {
         kload_all<TC>(kn, a.ks[i], l, t);
       }
+#endif
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
       fft_line<LN, false, HALF>(v, t, xb, tws);
+#if EIK_KPF
+      double kn[LN::EPT];
+      if (valid) kload_all<TC>(kn, a.ks[i], l, t);
+#endif
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r)
         v[r] = valid ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M) : make_double2(0.0, 0.0);
