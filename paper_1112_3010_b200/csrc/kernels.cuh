@@ -115,7 +115,10 @@ struct ColCfg {
 };
 // Row kernels (c2r / r2c along the contiguous last axis): complex lines of
 // length 2^LH = M_last/2, quarter table at the resolution of M_last.
-__host__ __device__ constexpr int row_e(int LH) { return LH >= 9 ? 8 : 16; }
+#ifndef EIK_ROW_E8_MIN
+#define EIK_ROW_E8_MIN 7
+#endif
+__host__ __device__ constexpr int row_e(int LH) { return LH >= EIK_ROW_E8_MIN ? 8 : 16; }
 template <int LH>
 struct RowCfg {
   using LN = PaddedLine<LH, row_e(LH), row_pad(LH)>;
