@@ -177,3 +177,73 @@ def test_gpu_classify_c2_full_size(cuda_ok):
     assert np.array_equal(got, ref)
     inside = got.mean()
     assert 0.2 < inside < 0.4  # star of radius ~600 in a 2048^2 grid
+
+
+# ----------------------------------------------------------------- empty / ragged / duplicate inputs
+
+
+@pytest.mark.parametrize("counts", [(48, 40), (12, 10, 9)])
+def test_empty_point_set(cuda_ok, counts):
+    """K = 0 is rejected with ValidationError, at the C ABI (eik_run: "empty
+    point set") and at the drop-in, where the reference cannot even build the
+    point set (R/grid.py:99-102).  An empty ITEM inside a batch is legal (see
+    test_ragged_batch_with_empty_item)."""
+    from paper_1112_3010_b200 import PointSet, ValidationError, engine
+
+    grid = _grid(counts)
+    dt = engine.DistanceTransform(grid, 1.0, grad=True)
+    with pytest.raises(ValidationError):
+        dt.run_host(np.zeros(0, dtype=np.int64))
+    with pytest.raises(ValueError):
+        PointSet(points=np.zeros((0, len(counts))), snapped_indices=np.zeros(0, dtype=np.int64))
+
+
+def test_ragged_batch_with_empty_item(cuda_ok):
+    """Items of different K, one of them empty, in one batched launch: each
+    item equals its own single-grid run bit for bit."""
+    from paper_1112_3010_b200 import engine
+
+    grid = _grid((64, 48))
+    rng = rng_for(77)
+    ks = [5, 0, 300, 1, 48]
+    nodes = [np.sort(rng.choice(grid.num_nodes, k, replace=False)) for k in ks]
+    offs = np.cumsum([0] + ks)
+    dt = engine.DistanceTransform(grid, 1.5, grad=True, hess=True)
+    batch = dt.run_host(np.concatenate(nodes), item_offsets=offs)
+    N = grid.num_nodes
+    empty = slice(N, 2 * N)  # item 1 has no sources: phi = 0, S = NaN, every node underflows
+    assert np.isnan(batch["S"][empty]).all() and batch["underflow"][empty].all()
+    for i, nd in enumerate(nodes):
+        if not ks[i]:
+            continue
+        single = dt.run_host(nd)
+        sl = slice(i * N, (i + 1) * N)
+        assert np.array_equal(single["S"], batch["S"][sl], equal_nan=True)
+        for a in range(2):
+            assert np.array_equal(single["grad"][a], batch["grad"][a][sl], equal_nan=True)
+        for a in range(3):
+            assert np.array_equal(single["hess"][a], batch["hess"][a][sl], equal_nan=True)
+        ref = orc.run_config_unchecked(nd, grid.counts, 1.0, 1.5)
+        keep = ref["phi"] >= 1e-5 * ref["phi"].max()
+        assert (np.abs(single["S"] - ref["S"])[keep] / np.maximum(np.abs(ref["S"][keep]), 1)).max() <= 1e-9
+    assert batch["n_underflow"] == int(batch["underflow"].sum())
+
+
+def test_duplicate_points_collapse(cuda_ok):
+    """Duplicated (and unsnapped) points collapse to one unit impulse per
+    node, as PointSet.distinct_nodes does in the reference (R/grid.py:89-121)."""
+    from paper_1112_3010_b200 import GridSpec, PointSet, PrecisionConfig
+    from paper_1112_3010_b200.distance import s_fft
+    from paper_1112_3010_b200.grid import snap_points
+
+    grid = GridSpec((0.0, 0.0), 0.5, (40, 36))
+    pts = np.array([[3.0, 4.0], [3.1, 3.9], [3.0, 4.0], [10.2, 7.7], [10.0, 7.5]])
+    ps = snap_points(pts, grid)
+    assert ps.distinct_nodes().size == 2
+    s_dup = s_fft(ps, grid, PrecisionConfig.native64(0.4)).values
+    uniq = PointSet.from_node_indices(grid, ps.distinct_nodes())
+    s_one = s_fft(uniq, grid, PrecisionConfig.native64(0.4)).values
+    assert np.array_equal(s_dup, s_one)
+    ref = orc.run_config_unchecked(ps.distinct_nodes(), grid.counts, 0.5, 0.4)
+    keep = ref["phi"] >= 1e-5 * ref["phi"].max()  # T1 conditioning mask
+    assert (np.abs(s_dup - ref["S"])[keep] / np.maximum(np.abs(ref["S"][keep]), 1.0)).max() <= 1e-9
