@@ -166,6 +166,31 @@ int eik_slab_p2p_init(eik_plan* plan, int world, int rank, int64_t c0_local, int
                       int64_t* arena_bytes, void* ipc_handle);
 int eik_slab_p2p_connect(eik_plan* plan, void* const* peer_arenas, const void* ipc_handles);
 
+/* Extended-precision (double-double, ~106-bit) convolution (SURVEY.md §8(f)
+ * rank 4): the big-float path of R/convolution.py:67-143 with p = 106, used by
+ * the drop-in API for PrecisionConfig.bigfloat(tau, bits <= 106).  Fields:
+ * EIK_FIELD_PHI | EIK_FIELD_S [| EIK_FIELD_GRAD | EIK_FIELD_HESS (2-D)];
+ * axes up to 2048 nodes.  phi is returned as its (hi, lo) double pair; S,
+ * gradient and Hessian as float64 (the reference converts big-float ratios to
+ * float64, R/derivatives.py:165-170).  Host or device buffers (flags
+ * EIK_HOST_INPUTS / EIK_HOST_OUTPUTS); synchronous; EIK_CHECK_UNDERFLOW
+ * returns EIK_EUNDERFLOW when any phi <= 0. */
+typedef struct eik_dd_plan eik_dd_plan;
+typedef struct {
+  double* phi_hi;
+  double* phi_lo;
+  double* S;
+  double* grad[3];
+  double* hess[3];
+  uint8_t* underflow;
+  int64_t* n_underflow; /* host */
+} eik_dd_outputs;
+int eik_dd_plan_create(int dim, const int64_t* counts, double spacing, double tau, uint32_t fields, int device,
+                       eik_dd_plan** out);
+int eik_dd_plan_destroy(eik_dd_plan* plan);
+int eik_dd_run(eik_dd_plan* plan, const int64_t* nodes, int64_t n_nodes, const eik_dd_outputs* out, uint32_t flags,
+               void* stream);
+
 /* tau sweep (the kernel-reuse of R/experiments.py:74-109):
  * one plan caches exp(-|x|/tau_i) spectra for n_taus values; eik_run_sweep
  * transforms delta_Y once and writes S_i = -tau_i log phi_i for every tau

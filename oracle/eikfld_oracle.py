@@ -34,7 +34,7 @@ __all__ = [
     "hessian_2d_unchecked", "snap", "tangent_impulses", "flux_impulses",
     "winding_field", "degree_field", "classify", "s_direct", "direct_ratios",
     "winding_direct", "degree_direct", "hessian_factors", "OracleUnderflow",
-    "run_config_unchecked",
+    "run_config_unchecked", "phi_direct_mp",
 ]
 
 
@@ -436,4 +436,34 @@ def run_config_unchecked(nodes, counts, spacing, tau, want_hessian=False):
     if want_hessian:
         hden, sxx, syy, sxy = hessian_2d_unchecked(nodes, counts, spacing, tau)
         out.update(hess_den=hden, hess=[sxx, syy, sxy])
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Extended-precision checker for the double-double path
+
+
+def phi_direct_mp(nodes, counts, spacing, tau, dps=60):
+    """phi(x) = sum_y exp(-h |i_x - i_y| / tau) over the distinct source nodes,
+    every term in mpmath at `dps` digits; returns log10(phi) per node (float64).
+
+    The exact value the big-float FFT path of the reference approximates
+    (R/distance.py:38-45 samples exp(-sqrt(q) * (h / tau)) at integer q; the
+    convolution sums those samples).  Pure Python: small grids only.
+    """
+    import mpmath
+
+    counts = tuple(int(c) for c in counts)
+    nodes = np.asarray(nodes, dtype=np.int64)
+    idx = np.stack(np.unravel_index(np.arange(int(np.prod(counts))), counts), axis=1)
+    src = idx[nodes]
+    out = np.empty(idx.shape[0])
+    with mpmath.workdps(dps):
+        scale = mpmath.mpf(spacing) / mpmath.mpf(tau)
+        for n in range(idx.shape[0]):
+            q = ((src - idx[n]) ** 2).sum(axis=1)
+            acc = mpmath.mpf(0)
+            for qq in q:
+                acc += mpmath.exp(-mpmath.sqrt(int(qq)) * scale)
+            out[n] = float(mpmath.log10(acc))
     return out

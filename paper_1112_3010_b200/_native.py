@@ -70,6 +70,10 @@ def lib():
             L.eik_slab_p2p_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
                                              C.c_void_p, C.c_void_p]
             L.eik_slab_p2p_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.eik_dd_plan_create.argtypes = [C.c_int, _i64p, C.c_double, C.c_double, C.c_uint32, C.c_int,
+                                              C.POINTER(C.c_void_p)]
+            L.eik_dd_plan_destroy.argtypes = [C.c_void_p]
+            L.eik_dd_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32, C.c_void_p]
             L.eik_plan_create_sweep.argtypes = [C.c_int, _i64p, C.c_double, _f64p, C.c_int, C.c_int,
                                                 C.POINTER(C.c_void_p)]
             L.eik_run_sweep.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint32,
@@ -87,7 +91,8 @@ def lib():
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
                          "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
                          "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep",
-                         "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect"):
+                         "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect", "eik_dd_plan_create",
+                         "eik_dd_plan_destroy", "eik_dd_run"):
                 getattr(L, name).restype = C.c_int
             _lib = L
         return _lib
@@ -97,6 +102,7 @@ def exported_symbols():
     return ["eik_plan_create", "eik_plan_create_slab", "eik_plan_destroy", "eik_plan_info", "eik_run",
             "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
             "eik_plan_create_sweep", "eik_run_sweep", "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect",
+            "eik_dd_plan_create", "eik_dd_plan_destroy", "eik_dd_run",
             "eik_last_error", "eik_version"]
 
 
@@ -290,6 +296,74 @@ def convolve(counts, kernels, field, device=0):
     check(lib().eik_convolve(len(counts), cnt, kernels.ctypes.data, n, ks, field.ctypes.data, out.ctypes.data,
                              HOST_INPUTS | HOST_OUTPUTS, device, None))
     return out
+
+
+class DDOutputs(C.Structure):
+    _fields_ = [("phi_hi", C.c_void_p), ("phi_lo", C.c_void_p), ("S", C.c_void_p), ("grad", C.c_void_p * 3),
+                ("hess", C.c_void_p * 3), ("underflow", C.c_void_p), ("n_underflow", C.c_void_p)]
+
+
+class DDPlan:
+    """Double-double (~106-bit) convolution plan: the big-float path of the
+    reference (R/convolution.py:67-143) with p = 106."""
+
+    def __init__(self, dim, counts, spacing, tau, fields, device=0):
+        self.dim = int(dim)
+        self.counts = tuple(int(c) for c in counts)
+        self.N = int(np.prod(self.counts))
+        h = C.c_void_p()
+        cnt = (C.c_int64 * 3)(*self.counts, *([1] * (3 - len(self.counts))))
+        check(lib().eik_dd_plan_create(self.dim, cnt, float(spacing), float(tau), int(fields), int(device),
+                                       C.byref(h)))
+        self._h = h
+        self._lock = threading.Lock()
+
+    def run(self, nodes, *, phi_hi=None, phi_lo=None, S=None, grad=(None, None, None), hess=(None, None, None),
+            underflow=None, check_underflow=False):
+        """Host arrays in and out; returns the number of nodes with phi <= 0."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+        o = DDOutputs()
+        o.phi_hi, o.phi_lo, o.S, o.underflow = (_ptr(x) for x in (phi_hi, phi_lo, S, underflow))
+        for d in range(3):
+            o.grad[d] = _ptr(grad[d]) if d < len(grad) else None
+            o.hess[d] = _ptr(hess[d]) if d < len(hess) else None
+        n_uf = C.c_int64(-1)
+        o.n_underflow = C.addressof(n_uf)
+        flags = HOST_INPUTS | HOST_OUTPUTS | SYNC | (CHECK_UNDERFLOW if check_underflow else 0)
+        with self._lock:
+            rc = lib().eik_dd_run(self._h, _ptr(nodes), int(nodes.shape[0]), C.byref(o), flags, None)
+        check(rc)
+        return n_uf.value
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._h = C.c_void_p()
+            try:
+                lib().eik_dd_plan_destroy(h)
+            except Exception:
+                pass
+
+    __del__ = close
+
+
+_DD_PLANS: "OrderedDict" = OrderedDict()
+
+
+def get_dd_plan(grid, tau, fields, device=0) -> DDPlan:
+    key = (device, tuple(grid.counts), float(grid.spacing), float(tau), int(fields))
+    with _PLANS_LOCK:
+        p = _DD_PLANS.get(key)
+        if p is not None:
+            _DD_PLANS.move_to_end(key)
+            return p
+    p = DDPlan(len(grid.counts), grid.counts, grid.spacing, tau, fields, device)
+    with _PLANS_LOCK:
+        _DD_PLANS[key] = p
+        while len(_DD_PLANS) > 2:  # DD plans are large (32 B per padded point per kernel)
+            _, old = _DD_PLANS.popitem(last=False)
+            old.close()
+    return p
 
 
 class SweepPlan(Plan):

@@ -16,7 +16,7 @@ from . import _native
 from .distance import _UNDERFLOW_MSG, distinct_nodes
 from .errors import PrecisionError, ValidationError
 from .grid import ScalarField, VectorField
-from .precision import require_native
+from .precision import arithmetic
 
 
 def _method(method):
@@ -32,9 +32,10 @@ def _method(method):
 def gradient(ps, grid, cfg, method: str = "fft") -> VectorField:
     """S_a = (f_a exp * delta)/(exp * delta); flagged = distinct source nodes."""
     _method(method)
-    tau = require_native(cfg)
+    mode, tau = arithmetic(cfg)
     nodes = distinct_nodes(ps, grid)
-    plan = _native.get_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S | _native.FIELD_GRAD)
+    fields = _native.FIELD_PHI | _native.FIELD_S | _native.FIELD_GRAD
+    plan = _native.get_dd_plan(grid, tau, fields) if mode == "dd" else _native.get_plan(grid, tau, fields)
     comps = [np.empty(grid.num_nodes) for _ in range(len(grid.counts))]
     try:
         plan.run(nodes, grad=comps, check_underflow=True)
@@ -48,9 +49,10 @@ def hessian_2d(ps, grid, cfg, method: str = "fft"):
     if len(grid.counts) != 2:
         raise ValidationError("second derivatives are implemented for 2D grids")
     _method(method)
-    tau = require_native(cfg)
+    mode, tau = arithmetic(cfg)
     nodes = distinct_nodes(ps, grid)
-    plan = _native.get_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S | _native.FIELD_GRAD | _native.FIELD_HESS)
+    fields = _native.FIELD_PHI | _native.FIELD_S | _native.FIELD_GRAD | _native.FIELD_HESS
+    plan = _native.get_dd_plan(grid, tau, fields) if mode == "dd" else _native.get_plan(grid, tau, fields)
     h = [np.empty(grid.num_nodes) for _ in range(3)]
     try:
         plan.run(nodes, hess=h, check_underflow=True)

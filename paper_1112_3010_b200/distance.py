@@ -14,7 +14,7 @@ import numpy as np
 from . import _native
 from .errors import PrecisionError, ValidationError
 from .grid import ScalarField
-from .precision import log_bound, require_native
+from .precision import arithmetic, log_bound, require_native
 
 _UNDERFLOW_MSG = (
     "{what} has non-positive entries after convolution; increase the precision bits "
@@ -59,11 +59,19 @@ def impulse_field(ps, grid) -> ScalarField:
 
 
 def _run_phi_family(ps, grid, cfg, *, want_s: bool, what: str):
-    tau = require_native(cfg)
+    mode, tau = arithmetic(cfg)
     _check_grid(grid)
     nodes = distinct_nodes(ps, grid)
-    plan = _native.get_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S)
     out = np.empty(grid.num_nodes, dtype=np.float64)
+    if mode == "dd":  # big-float config: double-double convolution (R/convolution.py:67-143, p = 106)
+        plan = _native.get_dd_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S)
+        kw = {"S": out} if want_s else {"phi_hi": out}
+        try:
+            plan.run(nodes, check_underflow=True, **kw)
+        except PrecisionError:
+            raise PrecisionError(_UNDERFLOW_MSG.format(what=what)) from None
+        return out
+    plan = _native.get_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S)
     kw = {"S": out} if want_s else {"phi": out}
     try:
         plan.run(nodes, check_underflow=True, **kw)
@@ -77,13 +85,15 @@ def phi_fft(ps, grid, cfg, convolver=None, kernel_hat=None) -> ScalarField:
 
     `convolver`/`kernel_hat` are accepted for signature compatibility; kernel
     spectra are always reused through the plan cache (the reference's reuse hook).
+    For big-float configs phi comes from the double-double convolution and is
+    returned rounded to float64 (the reference returns mpfr objects).
     """
     return ScalarField(grid, _run_phi_family(ps, grid, cfg, want_s=False, what="phi"))
 
 
 def s_from_phi(phi: ScalarField, cfg) -> ScalarField:
     """S = -tau log(phi) for a given phi field (R/distance.py:89-111)."""
-    tau = require_native(cfg)
+    _, tau = arithmetic(cfg)
     vals = np.asarray(phi.values, dtype=np.float64)
     if (vals <= 0).any():
         raise PrecisionError("phi <= 0: native64 underflow; rerun with --precision big:<bits>")

@@ -40,13 +40,19 @@ def test_precision_config():
         P.PrecisionConfig.parse("quad", 0.1)
 
 
-def test_bigfloat_rejected_without_fallback():
-    from paper_1112_3010_b200 import distance
+def test_bigfloat_wider_than_double_double_rejected():
+    """bits <= 106 run the double-double path (GPU); wider big-float configs are
+    rejected before any device work (no CPU fallback, no silent downgrade)."""
+    from paper_1112_3010_b200 import derivatives, distance
+    from paper_1112_3010_b200.precision import DD_BITS, arithmetic
 
     grid = P.GridSpec((0.0,), 0.1, (8,))
     ps = P.PointSet.from_node_indices(grid, [3])
-    with pytest.raises(P.ValidationError, match="float64 only"):
-        distance.s_fft(ps, grid, P.PrecisionConfig.bigfloat(0.1, 128))
+    for fn in (distance.s_fft, distance.phi_fft, derivatives.gradient):
+        with pytest.raises(P.ValidationError, match="double-double"):
+            fn(ps, grid, P.PrecisionConfig.bigfloat(0.1, 128))
+    assert arithmetic(P.PrecisionConfig.bigfloat(0.1, DD_BITS)) == ("dd", 0.1)
+    assert arithmetic(P.PrecisionConfig.native64(0.1)) == ("f64", 0.1)
 
 
 def test_grid_and_snapping():

@@ -101,3 +101,14 @@ def test_oracle_raises_on_underflow():
     # tests/test_distance.py:117-122
     with pytest.raises(orc.OracleUnderflow, match="precision"):
         orc.s_fft([0], (32, 32), 0.1, 1e-4)
+
+
+def test_bigfloat_fixtures_match_direct_mp_sum():
+    """The reference's big-float FFT answers (p = 200, tests/golden/
+    make_golden_bigfloat.py) equal the exact direct sums of the sampled
+    kernel: the truth the double-double GPU path is checked against."""
+    for name in ("bigfloat_1d", "bigfloat_2d", "bigfloat_3d"):
+        g = load_golden(f"{name}.npz")
+        ref = orc.phi_direct_mp(g["nodes"], g["counts"], float(g["h"]), float(g["tau"]), dps=50)
+        assert np.abs(ref - g["log10_phi"]).max() <= 1e-12, name
+        assert g["log10_phi"].min() < -22  # far below the float64 round-off floor
