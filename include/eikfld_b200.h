@@ -54,6 +54,9 @@ extern "C" {
                                       (R/convolution.py:378-388 assert_positive) */
 #define EIK_PROFILE 0x10u          /* record CUDA events around each pass (see eik_pass_times) */
 #define EIK_SLAB_P2P 0x20u         /* slab passes: exchange through peer arenas (eik_slab_p2p_*) */
+#define EIK_ASYNC 0x40u            /* host outputs: return once queued (no host sync, no result checks);
+                                      the outputs are complete when the stream is; consecutive calls on
+                                      one plan overlap the next column passes with this D2H */
 
 /* pass ids reported by eik_pass_times */
 #define EIK_PASS_PREP 0     /* node validation + per-row CSR */

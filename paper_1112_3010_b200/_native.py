@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 EIK_OK, EIK_EVALIDATION, EIK_EUNDERFLOW, EIK_ECUDA = 0, 1, 2, 3
 FIELD_PHI, FIELD_S, FIELD_GRAD, FIELD_HESS, FIELD_WINDING, FIELD_DEGREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
-HOST_INPUTS, HOST_OUTPUTS, SYNC, CHECK_UNDERFLOW, PROFILE, SLAB_P2P = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+HOST_INPUTS, HOST_OUTPUTS, SYNC, CHECK_UNDERFLOW, PROFILE, SLAB_P2P, ASYNC = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 PASS_NAMES = ("prep", "col", "col_sign", "lines", "row")
 
 _i64p = C.POINTER(C.c_int64)
@@ -217,8 +217,13 @@ class Plan:
 
     def run(self, nodes=None, item_offsets=None, batch=1, sign_nodes=None, sign_weights=None, *,
             phi=None, S=None, grad=(None, None, None), hess=(None, None, None), mu=None, mask=None,
-            underflow=None, count=False, check_underflow=False, host=True, stream=None, profile=False):
-        """Run the hot path.  Arrays are numpy (host=True) or torch CUDA tensors (host=False)."""
+            underflow=None, count=False, check_underflow=False, host=True, stream=None, profile=False,
+            wait=True):
+        """Run the hot path.  Arrays are numpy (host=True) or torch CUDA tensors (host=False).
+
+        host=True, wait=False queues the run and returns (EIK_ASYNC): outputs are
+        complete once `stream` is; the next run's column passes overlap this D2H.
+        """
         inp = Inputs()
         keep = []
         if nodes is not None:
@@ -247,6 +252,8 @@ class Plan:
             flags |= CHECK_UNDERFLOW
         if profile:
             flags |= PROFILE
+        if host and not wait:
+            flags |= ASYNC
         with self._lock:
             rc = lib().eik_run(self._h, C.byref(inp), C.byref(out), flags, stream)
         check(rc)

@@ -127,7 +127,8 @@ struct eik_plan {
   bool ev_used[EIK_NPASS] = {};
   // side stream: the 2-D sign group runs concurrently with the distance group
   cudaStream_t st2 = nullptr, st_copy = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr, ev_copies = nullptr;
+  bool copies_pending = false;  // EIK_ASYNC: D2H of the last run still reads `stage`
   DevBuf serr, trows, tsign;
   // peer-to-peer slab exchange: own arena [P2P_NV V slots][n_comp W slots]
   // and every rank's arena base (own, same-process or IPC-opened)
@@ -145,6 +146,7 @@ struct eik_plan {
     if (st2) cudaStreamDestroy(st2);
     if (st_copy) cudaStreamDestroy(st_copy);
     if (ev_chunk) cudaEventDestroy(ev_chunk);
+    if (ev_copies) cudaEventDestroy(ev_copies);
   }
 
   int64_t comp_elems() const {  // complex elements of one component of one item
@@ -937,11 +939,20 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     if (!out->d_underflow_count) CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     ra.uf_count = ctr;
   }
+  // EIK_ASYNC (host outputs): return without synchronising; the next run's
+  // column passes overlap this run's D2H, its row pass waits for it (stage reuse)
+  const bool async = (flags & EIK_ASYNC) && host_out && !(flags & (EIK_SYNC | EIK_CHECK_UNDERFLOW)) &&
+                     !out->n_underflow;
+  if (p->copies_pending) {
+    CK(cudaStreamWaitEvent(st, p->ev_copies, 0));
+    p->copies_pending = false;
+  }
   if (host_out && !slots.empty() && !prof && NB >= (int64_t(1) << 22)) {
     // D2H of each finished chunk of rows on a copy stream, overlapping the rest
     // of the row pass (the end-to-end path is PCIe-bound on the outputs)
     if (!p->st_copy) CK(cudaStreamCreateWithFlags(&p->st_copy, cudaStreamNonBlocking));
     if (!p->ev_chunk) CK(cudaEventCreateWithFlags(&p->ev_chunk, cudaEventDisableTiming));
+    if (!p->ev_copies) CK(cudaEventCreateWithFlags(&p->ev_copies, cudaEventDisableTiming));
     const int64_t nlast = p->c[p->D - 1];
     const int64_t item_nodes = p->N;
     ChunkFn on_chunk = [&](int64_t r0, int64_t r1, int64_t i0, int64_t i1) -> int {
@@ -958,15 +969,16 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
       return EIK_OK;
     };
     if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark, on_chunk))) return rc;
-    CK(cudaEventRecord(p->ev_chunk, p->st_copy));
-    CK(cudaStreamWaitEvent(st, p->ev_chunk, 0));
+    CK(cudaEventRecord(p->ev_copies, p->st_copy));
+    if (async) p->copies_pending = true;
+    else CK(cudaStreamWaitEvent(st, p->ev_copies, 0));
     slots.clear();
   } else {
     if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark))) return rc;
   }
   // ---- copy back / sync / checks
   for (auto& s : slots) CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));
-  const bool sync = host_out || (flags & (EIK_SYNC | EIK_CHECK_UNDERFLOW)) || out->n_underflow;
+  const bool sync = (host_out && !async) || (flags & (EIK_SYNC | EIK_CHECK_UNDERFLOW)) || out->n_underflow;
   int err_flag = 0;
   unsigned long long nuf = 0;
   if (sync) {
