@@ -126,7 +126,7 @@ struct eik_plan {
   cudaEvent_t ev[2 * EIK_NPASS] = {};
   bool ev_used[EIK_NPASS] = {};
   // side stream: the 2-D sign group runs concurrently with the distance group
-  cudaStream_t st2 = nullptr, st_copy = nullptr;
+  cudaStream_t st2 = nullptr, st_copy = nullptr, st_copy2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr, ev_copies = nullptr;
   bool copies_pending = false;  // EIK_ASYNC: D2H of the last run still reads `stage`
   DevBuf serr, trows, tsign;
@@ -145,6 +145,7 @@ struct eik_plan {
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
     if (st_copy) cudaStreamDestroy(st_copy);
+    if (st_copy2) cudaStreamDestroy(st_copy2);
     if (ev_chunk) cudaEventDestroy(ev_chunk);
     if (ev_copies) cudaEventDestroy(ev_copies);
   }
@@ -950,7 +951,9 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
   if (host_out && !slots.empty() && !prof && NB >= (int64_t(1) << 22)) {
     // D2H of each finished chunk of rows on a copy stream, overlapping the rest
     // of the row pass (the end-to-end path is PCIe-bound on the outputs)
+    // two copy streams: consecutive copies alternate between copy engines
     if (!p->st_copy) CK(cudaStreamCreateWithFlags(&p->st_copy, cudaStreamNonBlocking));
+    if (!p->st_copy2) CK(cudaStreamCreateWithFlags(&p->st_copy2, cudaStreamNonBlocking));
     if (!p->ev_chunk) CK(cudaEventCreateWithFlags(&p->ev_chunk, cudaEventDisableTiming));
     if (!p->ev_copies) CK(cudaEventCreateWithFlags(&p->ev_copies, cudaEventDisableTiming));
     const int64_t nlast = p->c[p->D - 1];
@@ -958,17 +961,22 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     ChunkFn on_chunk = [&](int64_t r0, int64_t r1, int64_t i0, int64_t i1) -> int {
       CK(cudaEventRecord(p->ev_chunk, st));
       CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
+      CK(cudaStreamWaitEvent(p->st_copy2, p->ev_chunk, 0));
+      int k = 0;
       for (auto& sl : slots) {
         const size_t elem = sl.bytes / (size_t)NB;
         for (int64_t it = i0; it < i1; ++it) {
           const size_t off = ((size_t)it * item_nodes + (size_t)r0 * nlast) * elem;
           const size_t len = (size_t)(r1 - r0) * nlast * elem;
-          CK(cudaMemcpyAsync((char*)sl.user + off, (char*)sl.dev + off, len, cudaMemcpyDeviceToHost, p->st_copy));
+          CK(cudaMemcpyAsync((char*)sl.user + off, (char*)sl.dev + off, len, cudaMemcpyDeviceToHost,
+                             (k++ & 1) ? p->st_copy2 : p->st_copy));
         }
       }
       return EIK_OK;
     };
     if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark, on_chunk))) return rc;
+    CK(cudaEventRecord(p->ev_chunk, p->st_copy2));
+    CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
     CK(cudaEventRecord(p->ev_copies, p->st_copy));
     if (async) p->copies_pending = true;
     else CK(cudaStreamWaitEvent(st, p->ev_copies, 0));
