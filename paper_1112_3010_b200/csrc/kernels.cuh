@@ -260,6 +260,24 @@ __device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t) 
     }
   }
 }
+// v[r] *= K (all EPT registers of this thread): the real / imaginary and fold-
+// sign cases are uniform per kernel, so they are branched on once, not selected
+// per element.
+template <class LN>
+__device__ __forceinline__ void kapply_all(double2 (&v)[LN::EPT], double (&kv)[LN::EPT], const KSpec& k, int t) {
+  if (k.odd0) {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r)
+      if (LN::out_idx(t, r) > (LN::M >> 1)) kv[r] = -kv[r];
+  }
+  if (k.imag) {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(-v[r].y * kv[r], v[r].x * kv[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(v[r].x * kv[r], v[r].y * kv[r]);
+  }
+}
 __device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0) {
   if (k.odd0 && k0 > (M0 >> 1)) v = -v;
   return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
@@ -509,9 +527,12 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       double kn[LN::EPT];
       if (valid) kload_all<TC>(kn, a.ks[i], l, t);
 #endif
+      if (valid) {
+        kapply_all<LN>(v, kn, a.ks[i], t);
+      } else {
 #pragma unroll
-      for (int r = 0; r < LN::EPT; ++r)
-        v[r] = valid ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M) : make_double2(0.0, 0.0);
+        for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(0.0, 0.0);
+      }
       if (i > 0) {
         double2 y[LN::EPT];
         tmem_get(ta, y);
@@ -545,8 +566,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       double kn[LN::EPT];
       kload_all<TC>(kn, a.ks[j], l, t);
       if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], l, t);
-#pragma unroll
-      for (int r = 0; r < LN::EPT; ++r) v[r] = kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M);
+      kapply_all<LN>(v, kn, a.ks[j], t);
     }
 #else
   double kn[LN::EPT];
