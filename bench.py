@@ -167,12 +167,7 @@ class ClockSampler:
 
             def poll():
                 while not self.stop.is_set():
-                    try:
-                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        self.samples.append((sm, self.max_mhz, rs))
-                    except Exception:
-                        pass
+                    self.sample()
                     time.sleep(0.001)
 
             self.t = threading.Thread(target=poll, daemon=True)
@@ -182,7 +177,20 @@ class ClockSampler:
             self.nv = None
         return self
 
+    def sample(self):
+        try:
+            nv, h = self.nv, self.h
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((sm, self.max_mhz, rs))
+        except Exception:
+            pass
+
     def __exit__(self, *exc):
+        # one synchronous sample at the end of the region as well (the poller
+        # can be starved of the GIL while the timed loop enqueues)
+        if self.nv is not None:
+            self.sample()
         self.stop.set()
         if self.nv is not None:
             self.t.join(timeout=2)
@@ -353,6 +361,7 @@ def main():
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
+            clk.sample()  # host-side, while the step runs on the device
         torch.cuda.synchronize()
     total_ms = sum(s.elapsed_time(e) for s, e in ev)
     if dist:
@@ -539,6 +548,7 @@ def bench_sweep(a):
         e0.record(stream)
         for _ in range(a.steps):
             plan.run_sweep(nd, outs, host=False, stream=stream.cuda_stream)
+            clk.sample()
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
@@ -608,6 +618,7 @@ def bench_c4(a):
             ev[i][0].record(stream)
             out = run_rank(ex, exchange, ln_d, lsn_d, lsw_d)
             ev[i][1].record(stream)
+            clk.sample()
         torch.cuda.synchronize()
     total_ms = sum(s_.elapsed_time(e_) for s_, e_ in ev)
     if dist:
