@@ -30,6 +30,10 @@
 
 namespace eik {
 
+#ifndef EIK_TW_POW
+#define EIK_TW_POW 1
+#endif
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 // a * w
@@ -340,10 +344,23 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
         }
       }
       if (!done) {
+        if constexpr (EIK_TW_POW && LN::TWO_LEVEL && R > 2) {
+          // radix <= 8 lines: W^{k r} as powers of W^k (one table lookup per
+          // group instead of R-1, or 2(R-1) for two-level stages); products in
+          // registers trade shared-memory wavefronts for FP64 issue
+          const double2 w1 = st_tw<LN, INV, S>(tw, k, 1);
+          double2 w = w1;
 #pragma unroll
-        for (int r = 1; r < R; ++r) {
-          const double2 w = st_tw<LN, INV, S>(tw, k, r);
-          v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
+          for (int r = 1; r < R; ++r) {
+            if (r > 1) w = cmul(w, w1);
+            v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
+          }
+        } else {
+#pragma unroll
+          for (int r = 1; r < R; ++r) {
+            const double2 w = st_tw<LN, INV, S>(tw, k, r);
+            v[g * R + r] = INV ? cmulc(v[g * R + r], w) : cmul(v[g * R + r], w);
+          }
         }
       }
     }
