@@ -77,3 +77,44 @@ def test_dd_validation(cuda_ok):
     ps = PointSet.from_node_indices(grid, [0])
     with pytest.raises(ValidationError):  # axes up to 2048 nodes
         s_fft(ps, grid, PrecisionConfig.bigfloat(1.0, 106))
+
+
+# Mirrors of the reference's big-float unit tests at double-double precision
+# (R/../tests/test_distance.py:79-89, 179-189; there at p = 192, here p = 106).
+
+
+def _nodes(grid, seed, k):
+    return np.sort(np.random.Generator(np.random.PCG64(seed)).choice(grid.num_nodes, k, replace=False))
+
+
+def test_k1_recovers_distance_bigfloat(cuda_ok):
+    """One source at the centre of a 20 x 20 grid, tau = 0.02: S equals the
+    exact Euclidean distance to 1e-12 (R/tests/test_distance.py:87-89)."""
+    from paper_1112_3010_b200 import GridSpec, PointSet, PrecisionConfig
+    from paper_1112_3010_b200.distance import s_fft
+
+    grid = GridSpec((0.0, 0.0), 0.05, (20, 20))
+    ps = PointSet.from_node_indices(grid, [10 * 20 + 10])
+    s = s_fft(ps, grid, PrecisionConfig.bigfloat(0.02, 106)).values
+    ij = np.stack(np.unravel_index(np.arange(400), (20, 20)), axis=1)
+    r = 0.05 * np.sqrt(((ij - np.array([10, 10])) ** 2).sum(axis=1))
+    assert np.abs(s - r).max() < 1e-12
+
+
+@pytest.mark.parametrize("counts", [(40,), (12, 14), (6, 7, 8)])
+def test_dimension_independence_bigfloat(cuda_ok, counts):
+    """Same pipeline for D = 1, 2, 3 against the stable direct soft-min
+    (R/tests/test_distance.py:179-189, tolerance 1e-11)."""
+    import eikfld_oracle as orc
+
+    from paper_1112_3010_b200 import GridSpec, PointSet, PrecisionConfig
+    from paper_1112_3010_b200.distance import s_fft
+
+    origin = tuple(0.0 for _ in counts)
+    grid = GridSpec(origin, 0.02, counts)
+    nodes = _nodes(grid, 21, 5)
+    ps = PointSet.from_node_indices(grid, nodes)
+    s = s_fft(ps, grid, PrecisionConfig.bigfloat(0.05, 106)).values
+    pts = np.stack(np.unravel_index(nodes, counts), axis=1) * 0.02
+    direct = orc.s_direct(pts, origin, 0.02, counts, 0.05)
+    assert np.abs(s - direct).max() < 1e-11
