@@ -1,7 +1,7 @@
 # Builds the in-tree CUDA library for sm_100a (B200) and the oracle's C helpers.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v $(EXTRA)
 SRC := paper_1112_3010_b200/csrc
 OBJ := build/obj
 LIB := paper_1112_3010_b200/_lib/libeikfld_b200.so

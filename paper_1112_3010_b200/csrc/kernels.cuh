@@ -178,6 +178,7 @@ struct ColArgs {
   // dense input din[i][item*din_item + e*din_es + l]
   const double2* din[3];
   int64_t din_es, din_item;
+  int64_t din_ls;  // line stride of the dense input (1: lines are adjacent columns)
   // kernel spectra (COMPS: one per component; SUM: one per input)
   KSpec ks[MAXC];
   // outputs out[j][item*out_item + n*out_es + l]
@@ -193,6 +194,7 @@ struct ColArgs {
   int64_t spec_ld;
   const double2* tw;
   int lmax;
+  int kfeed;  // set by the launcher: shared-memory feed of register-order kernel spectra
   // Peer-block outputs (slab exchange fused into the pass, P2P over NVLink):
   // when blk[0] is set, output row n of component j is written to
   // blk[n >> blk_shift] + j * blk_cstride + item * out_item + (n mod 2^blk_shift) * out_es + l,
@@ -327,7 +329,7 @@ __device__ __forceinline__ void load_sparse(double2 (&v)[LN::EPT], const ColArgs
 template <class LN, bool HALF>
 __device__ __forceinline__ void load_dense(double2 (&v)[LN::EPT], const ColArgs& a, int t, int64_t l,
                                            int64_t item, int inp, bool valid) {
-  const double2* __restrict__ src = a.din[inp] + item * a.din_item + l;
+  const double2* __restrict__ src = a.din[inp] + item * a.din_item + l * a.din_ls;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
     if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
@@ -450,10 +452,17 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 // Four-step 4096-point lines of the multi-component (COMPS) kernel: EIK_F4K_LPC
 // lines per CTA, interleaved by lane parity, so warp loads/stores cover two
 // adjacent columns (one CTA per SM).  The SUM kernel (sign group: two forward
-// transforms, one inverse) keeps one line per CTA: measured faster there.
+// transforms, one inverse) does the same (measured 186 -> 180 us at C2: its
+// T reads become whole 32-byte sectors).
+#ifndef EIK_F4K_LPC_SUM
+#define EIK_F4K_LPC_SUM 2
+#endif
 __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
-  return (L == 12 && EIK_FOUR_STEP && OUT == OUT_COMPS) ? EIK_F4K_LPC : 1;
+  return (L == 12 && EIK_FOUR_STEP) ? (OUT == OUT_COMPS ? EIK_F4K_LPC : OUT == OUT_SUM ? EIK_F4K_LPC_SUM : 1) : 1;
 }
+#ifndef EIK_KFEED
+#define EIK_KFEED 0
+#endif
 template <int L, int LPCX = 1>
 struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
@@ -474,6 +483,13 @@ struct TmCfg {
   static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
+  // Kernel-spectrum feed (register-order spectra, 2-D plans): the CTA's whole
+  // block of the next component's spectrum (EPT x NT doubles, contiguous) is
+  // bulk-copied into shared memory one transform ahead, where it fits next to
+  // MINB resident CTAs (C2: 64 KB on top of 158 KB, one CTA per SM).
+  static constexpr size_t KFEED_BYTES = (size_t)LN::EPT * NT * sizeof(double);
+  static constexpr bool KFEED = EIK_KFEED && (SMEM_BYTES + 16 + KFEED_BYTES) * MINB <= 227 * 1024;
+  static constexpr size_t SMEM_FEED_BYTES = SMEM_BYTES + (KFEED ? 16 + KFEED_BYTES : 0);
 };
 
 template <int L, int IN, int OUT, bool HALF>
@@ -494,6 +510,10 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   uint32_t* slot = reinterpret_cast<uint32_t*>(sts + LN::ST_SIZE);
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
+  if (TC::KFEED && a.kfeed && OUT == OUT_COMPS && threadIdx.x == 0) {
+    mbar_init(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle tables
   const uint32_t ta = tmem_thread_addr(tbase, TC::WPT_ALL);
   uint32_t ttw = 0;
@@ -551,10 +571,44 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     tmem_free_cta(tbase, TC::COLS);
     return;
   }
+  // kernel-spectrum feed (TC::KFEED, launched with a.kfeed): bar + buffer after the base layout
+  uint64_t* kbar = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES);
+  double* kbuf = reinterpret_cast<double*>(kbar + 2);
+  const bool kfeed = TC::KFEED && a.kfeed;
+  auto kfeed_issue = [&](int j) {
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(kbar, (uint32_t)TC::KFEED_BYTES);
+      bulk_g2s(kbuf, a.ks[j].perm + (int64_t)blockIdx.x * LN::EPT * TC::NT, (uint32_t)TC::KFEED_BYTES, kbar);
+    }
+  };
+  if (kfeed) kfeed_issue(0);  // lands while the input line is loaded and transformed
   if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
   else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
   fft_line<LN, false, HALF>(v, t, xb, tws);
   tmem_put(ta, v);
+  if (kfeed) {
+#pragma unroll 1
+    for (int j = 0; j < a.n_comp; ++j) {
+      tmem_get(ta, v);
+      double kn[LN::EPT];
+      mbar_wait(kbar, (uint32_t)(j & 1));
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) kn[r] = kbuf[r * TC::NT + threadIdx.x];
+      __syncthreads();  // every thread has its values: the buffer may be refilled
+      if (j + 1 < a.n_comp) kfeed_issue(j + 1);
+      if (valid) kapply_all<LN>(v, kn, a.ks[j], t);
+      fft_line<LN, true>(v, t, xb, tws);
+#pragma unroll
+      for (int r = 0; r < LN::EPT; ++r) {
+        if (LN::L > 0 && LN::upper_in(r)) continue;
+        const int n = LN::in_idx(t, r);
+        if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = v[r];
+      }
+    }
+    tmem_free_cta(tbase, TC::COLS);
+    return;
+  }
 #if EIK_KPF
   // kernel spectra: the next component's lines are prefetched into L1 one
   // transform ahead (no registers held across the FFT); loaded at use
@@ -895,7 +949,10 @@ __device__ __forceinline__ void c2r_twist(double2 (&z)[LN::EPT], const double2* 
   }
 }
 
-template <int LH>
+// RCP: the ratios u_c / phi are formed as u_c * (scale / phi) (launched for
+// plans with the Hessian, five ratios per node: measured C2 row -9%; with only
+// the gradient the extra clamp costs more than the two divisions it saves)
+template <int LH, bool RCP>
 __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(const __grid_constant__ RowArgs a) {
   using LN = typename RowCfg<LH>::LN;
   constexpr int LPC = RowCfg<LH>::LPC;
@@ -975,6 +1032,14 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
 
   double2 phi[E], sg[3][E];
   double2 z[E];
+  // RCP: after the S epilogue phi[] holds scale / phi (one division per node
+  // instead of one per component, no extra registers; <= 1.5 ulp instead of
+  // 0.5).  Nodes with phi below ~1e-300 of the scale (deep underflow: noise
+  // either way) get a clamped reciprocal.
+  auto ratio = [&](double2 u, int r) {
+    if constexpr (RCP) return make_double2(u.x * phi[r].x, u.y * phi[r].y);
+    else return make_double2((u.x * a.scale) / phi[r].x, (u.y * a.scale) / phi[r].y);
+  };
   // inverse real transform of component c's row into z (prefetching the next row)
   auto row_c2r = [&](const double2* X) {
     const double2* xs = row_src();
@@ -1001,6 +1066,9 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
         put(a.S, r, s0, s1);
       }
       if (a.uf) putb(a.uf, r, phi[r].x <= 0.0, phi[r].y <= 0.0);
+      if constexpr (RCP)
+        phi[r] = make_double2(fmin(fmax(a.scale / phi[r].x, -1e300), 1e300),
+                              fmin(fmax(a.scale / phi[r].y, -1e300), 1e300));
     }
   }
   if (a.c_grad >= 0) {
@@ -1010,7 +1078,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
-        const double2 q = make_double2((z[r].x * a.scale) / phi[r].x, (z[r].y * a.scale) / phi[r].y);
+        const double2 q = ratio(z[r], r);
         if (d == 0) sg[0][r] = q; else if (d == 1) sg[1][r] = q; else sg[2][r] = q;
         if (a.grad[d]) put(a.grad[d], r, q.x, q.y);
       }
@@ -1023,7 +1091,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
 #pragma unroll
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
-        const double2 tq = make_double2((z[r].x * a.scale) / phi[r].x, (z[r].y * a.scale) / phi[r].y);
+        const double2 tq = ratio(z[r], r);
         // xx: tq + (1/tau) sx sx, yy: tq + (1/tau) sy sy, xy: tq + (1/tau) sx sy (R/derivatives.py:102-106)
         const double2 u = (d == 1) ? sg[1][r] : sg[0][r];
         const double2 pw = (d == 0) ? sg[0][r] : sg[1][r];
@@ -1094,11 +1162,21 @@ struct RowDftArgs {
   int64_t rows_per_item, H;
   double2* out[3];
   int64_t out_item;  // complex elements per item (rows_per_item * H)
+  int64_t out_rs, out_ks;  // element (row, k) at row * out_rs + k * out_ks: (H, 1) row-major, (1, rows) transposed
   int last_shift, last_mask;
   const double2* tw;
 };
 
 constexpr int ROWDFT_NT = 256;
+// Transposed T ([k1][row]) for the 2-D groups in this mask: 1 = sign, 2 = distance
+// (measured: sign column kernel -22%, but one-row-per-CTA transposed writes
+// cost the impulse DFT more than that; off)
+#ifndef EIK_T_TRANSPOSE
+#define EIK_T_TRANSPOSE 0
+#endif
+#ifndef EIK_ROWDFT_SPLIT
+#define EIK_ROWDFT_SPLIT 1
+#endif
 constexpr int ROWDFT_NF = 16;     // max frequencies per thread (H <= ROWDFT_NF * ROWDFT_NT)
 constexpr int ROWDFT_STAGE = 1536;  // staged points per CTA and chunk (<= 42 KB of shared memory)
 
@@ -1155,10 +1233,21 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
       double wv[NIN];
 #pragma unroll
       for (int i = 0; i < NIN; ++i) wv[i] = ws[(i * rpb + rl) * ROWDFT_CHUNK + p];
+#if EIK_ROWDFT_SPLIT
+      // W^{col k} = W^{col tl} * W^{col q tpr}: one gathered table read per
+      // point (lane-dependent) and NF row-uniform (broadcast) reads, instead of
+      // NF gathers that touch one cache line per lane
+      const double2 wb = __ldg(a.tw + ((int)((col * tl) & a.last_mask) << a.last_shift));
+#endif
 #pragma unroll
       for (int q = 0; q < NF; ++q) {
+#if EIK_ROWDFT_SPLIT
+        const double2 t = q == 0 ? wb
+                                 : cmul(wb, __ldg(a.tw + ((int)((col * q * tpr) & a.last_mask) << a.last_shift)));
+#else
         const int64_t k = tl + (int64_t)q * tpr;
         const double2 t = __ldg(a.tw + ((int)((col * k) & a.last_mask) << a.last_shift));
+#endif
 #pragma unroll
         for (int i = 0; i < NIN; ++i) {
           acc[i][q].x = fma(wv[i], t.x, acc[i][q].x);
@@ -1178,15 +1267,20 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   if (!valid) return;
 #pragma unroll
   for (int i = 0; i < NIN; ++i) {
-    double2* dst = a.out[i] + item * a.out_item + row * a.H;
+    double2* dst = a.out[i] + item * a.out_item + row * a.out_rs;
 #pragma unroll
-    for (int q = 0; q < NF; ++q) dst[tl + (int64_t)q * tpr] = acc[i][q];
-    if (tl == 0) dst[half] = nyq[i];
+    for (int q = 0; q < NF; ++q) dst[(tl + (int64_t)q * tpr) * a.out_ks] = acc[i][q];
+    if (tl == 0) dst[half * a.out_ks] = nyq[i];
   }
 }
 
 // Launch the impulse DFT for n_in inputs over `rows` rows of `items` items.
-inline cudaError_t launch_impulse_rows(const RowDftArgs& ra, int n_in, int64_t rows, int64_t items, cudaStream_t st) {
+inline cudaError_t launch_impulse_rows(const RowDftArgs& ra_in, int n_in, int64_t rows, int64_t items, cudaStream_t st) {
+  RowDftArgs ra = ra_in;
+  if (ra.out_rs == 0) {  // default layout: row-major [row][k]
+    ra.out_rs = ra.H;
+    ra.out_ks = 1;
+  }
   const int nf = rowdft_nf(ra.H), tpr = rowdft_tpr(ra.H), rpb = ROWDFT_NT / tpr;
   const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
   const dim3 grid((unsigned)((rows + rpb - 1) / rpb), (unsigned)items);

@@ -16,11 +16,18 @@ template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
   using C = TmCfg<L, tm_lpcx(L, OUT)>;
   auto k = col_tmem_kernel<L, IN, OUT, HALF>;
-  CK(prep_kernel_attr(k, C::SMEM_BYTES));
+  CK(prep_kernel_attr(k, C::SMEM_FEED_BYTES));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
   if (tiles <= 0 || items <= 0) return EIK_OK;
   if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
-  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);
+  // kernel-spectrum feed: every component has a register-order spectrum of this configuration
+  ColArgs b = a;
+  b.kfeed = 0;
+  if (C::KFEED && OUT == OUT_COMPS && !a.blk[0]) {
+    b.kfeed = 1;
+    for (int j = 0; j < a.n_comp; ++j) b.kfeed &= (a.ks[j].perm != nullptr);
+  }
+  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, b.kfeed ? C::SMEM_FEED_BYTES : C::SMEM_BYTES, st>>>(b);
   CK(cudaGetLastError());
   return EIK_OK;
 }

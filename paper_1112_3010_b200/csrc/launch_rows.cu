@@ -3,7 +3,7 @@
 template <int LH>
 int launch_row_t(const RowArgs& a, int64_t items, cudaStream_t st) {
   using C = RowCfg<LH>;
-  auto k = row_kernel<LH>;
+  auto k = a.c_hess >= 0 ? row_kernel<LH, true> : row_kernel<LH, false>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
   const int64_t tiles = (a.row_end - a.row0 + C::LPC - 1) / C::LPC;
   if (tiles <= 0) return EIK_OK;

@@ -169,6 +169,7 @@ constexpr int NOSPLIT = 30;  // split shift meaning "no split"
 
 ColArgs col_defaults(const eik_plan* p) {
   ColArgs a{};
+  a.din_ls = 1;
   a.out_split_shift = NOSPLIT;
   a.out_split_stride = 0;
   a.tw = p->tw.as<double2>();
@@ -523,6 +524,12 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     ra.rows_per_item = p->c[0];
     ra.H = p->H;
     ra.out_item = per;
+    // T layout: [k1][row] (transposed) where the column kernel holds one line
+    // per CTA (the sign group): its warp loads are then contiguous runs of a
+    // column instead of one 16-byte half sector per row
+    const bool tt = (EIK_T_TRANSPOSE >> (sg ? 0 : 1)) & 1;
+    ra.out_rs = tt ? 1 : p->H;
+    ra.out_ks = tt ? p->c[0] : 1;
     ra.last_shift = p->lmax - p->L[1];
     ra.last_mask = p->M[1] - 1;
     ra.tw = p->tw.as<double2>();
@@ -533,7 +540,8 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     a.n_out = p->c[0];
     a.n_in = n_in;
     for (int i = 0; i < n_in; ++i) a.din[i] = ra.out[i];
-    a.din_es = p->H;
+    a.din_es = tt ? 1 : p->H;
+    a.din_ls = tt ? p->c[0] : 1;
     a.din_item = per;
     a.out_es = p->H;
     a.out_item = p->comp_elems();
