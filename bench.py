@@ -405,9 +405,10 @@ def main():
         ho["hess"] = [pinned(B * N, torch.float64) for _ in range(3)]
         d2h += 3 * B * N * 8
     if sn_h is not None:
-        ho["mu"] = pinned(N, torch.float64)
+        # the config's sign output is the inside/outside mask (classify's rint(mu) > 0);
+        # the winding number mu itself stays on the device in the e2e arm
         ho["mask"] = pinned(N, torch.uint8)
-        d2h += N * 9
+        d2h += N
     h2d = nodes_h.nbytes + (offs_h.nbytes if offs_h is not None else 16) + \
         ((sn_h.nbytes + sw_h.nbytes + 16) if sn_h is not None else 0)
 
@@ -484,7 +485,8 @@ def main():
                        "parallelism": "replicas" if a.config != "C5" else f"batch-shard x{world}",
                        "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": e2e_val, "unit": "grid_points/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "steps": ke},
+                    "d2h_bytes_per_step": int(d2h), "steps": ke,
+                    "outputs": [k for k in ("S", "grad", "hess", "mask") if k in ho]},
             "gpu_launches": launches_per_step * a.steps,
             "pass_ms": {k: round(v, 5) for k, v in mean_pass.items()},
             "phi_validity": validity,

@@ -206,7 +206,9 @@ class Plan:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if C is None or h is None:  # interpreter shutdown: module globals already gone
+            return
+        if h.value:
             self._h = C.c_void_p()
             try:
                 lib().eik_plan_destroy(h)
@@ -344,7 +346,9 @@ class DDPlan:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if C is None or h is None:  # interpreter shutdown: module globals already gone
+            return
+        if h.value:
             self._h = C.c_void_p()
             try:
                 lib().eik_dd_plan_destroy(h)

@@ -119,13 +119,16 @@ struct ColCfg {
 #define EIK_ROW_E8_MIN 7
 #endif
 __host__ __device__ constexpr int row_e(int LH) { return LH >= EIK_ROW_E8_MIN ? 8 : 16; }
+#ifndef EIK_ROW_NBUF2_MAX
+#define EIK_ROW_NBUF2_MAX 10
+#endif
 template <int LH>
 struct RowCfg {
   using LN = PaddedLine<LH, row_e(LH), row_pad(LH)>;
   static constexpr int NT = (LN::TPL >= 128) ? LN::TPL : 128;
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
-  static constexpr int NBUF = (LH <= 10 && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
+  static constexpr int NBUF = (LH <= EIK_ROW_NBUF2_MAX && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
   using XB = XBuf<NBUF, group_sync(1, LPC, LN::TPL), LN::TPL>;  // row kernels are line-major
   static constexpr size_t BASE_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
   // resident CTAs per SM requested from the register allocator (128 threads:
@@ -609,6 +612,35 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     tmem_free_cta(tbase, TC::COLS);
     return;
   }
+#if EIK_KPF == 2
+  // kernel spectra: component j+1's values are loaded into registers between
+  // the inverse transform of component j and its stores (the stores and the
+  // TMEM reload of X cover the load latency; v and kn are the only live
+  // arrays there), and warmed in L2 one transform ahead of that
+  double kn[LN::EPT];
+  if (valid) {
+    kload_all<TC>(kn, a.ks[0], l, t);
+    if (a.n_comp > 1) kprefetch_all<TC>(a.ks[1], l, t);
+  }
+#pragma unroll 1
+  for (int j = 0; j < a.n_comp; ++j) {
+    tmem_get(ta, v);
+    if (valid) {
+      kapply_all<LN>(v, kn, a.ks[j], t);
+      if (j + 2 < a.n_comp) kprefetch_all<TC>(a.ks[j + 2], l, t);
+    }
+    fft_line<LN, true>(v, t, xb, tws);
+    if (valid && j + 1 < a.n_comp) kload_all<TC>(kn, a.ks[j + 1], l, t);
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) {
+      if (LN::L > 0 && LN::upper_in(r)) continue;
+      const int n = LN::in_idx(t, r);
+      if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = v[r];
+    }
+  }
+  tmem_free_cta(tbase, TC::COLS);
+  return;
+#endif
 #if EIK_KPF
   // kernel spectra: the next component's lines are prefetched into L1 one
   // transform ahead (no registers held across the FFT); loaded at use
@@ -1163,6 +1195,7 @@ struct RowDftArgs {
   double2* out[3];
   int64_t out_item;  // complex elements per item (rows_per_item * H)
   int64_t out_rs, out_ks;  // element (row, k) at row * out_rs + k * out_ks: (H, 1) row-major, (1, rows) transposed
+  int npass;               // frequency passes per CTA (0 = 1)
   int last_shift, last_mask;
   const double2* tw;
 };
@@ -1173,6 +1206,9 @@ constexpr int ROWDFT_NT = 256;
 // cost the impulse DFT more than that; off)
 #ifndef EIK_T_TRANSPOSE
 #define EIK_T_TRANSPOSE 0
+#endif
+#ifndef EIK_T_NPASS
+#define EIK_T_NPASS 2
 #endif
 #ifndef EIK_ROWDFT_SPLIT
 #define EIK_ROWDFT_SPLIT 1
@@ -1189,7 +1225,10 @@ __host__ __device__ constexpr int rowdft_tpr(int64_t H) { return (int)((H - 1) /
 template <int NIN, int NF>
 __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_constant__ RowDftArgs a) {
   extern __shared__ double rowdft_smem[];
-  const int tpr = (int)((a.H - 1) / NF);
+  // a.npass passes over the frequencies, NF * tpr of them per pass: more rows
+  // per CTA (rpb) for the transposed layout, whose k-th output run is rpb rows
+  const int npass = a.npass;
+  const int tpr = (int)((a.H - 1) / (NF * npass));
   const int rpb = ROWDFT_NT / tpr;
   const int rl = threadIdx.x / tpr, tl = threadIdx.x % tpr;
   const int ROWDFT_CHUNK = ROWDFT_STAGE / rpb;  // per row
@@ -1203,13 +1242,6 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   const int64_t p0 = valid ? __ldg(a.rowptr + grow) : 0, p1 = valid ? __ldg(a.rowptr + grow + 1) : 0;
   const int nyq_shift = a.last_shift;  // W^{(col * M/2) mod M}: index 0 or M/2 of the M-point table
   const int64_t half = a.H - 1;
-  double2 acc[NIN][NF], nyq[NIN];
-#pragma unroll
-  for (int i = 0; i < NIN; ++i) {
-    nyq[i] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < NF; ++q) acc[i][q] = make_double2(0.0, 0.0);
-  }
   // rows of one CTA may differ in length: loop to the CTA's longest row
   __shared__ int s_maxlen;
   if (threadIdx.x == 0) s_maxlen = 0;
@@ -1217,60 +1249,75 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   if (tl == 0) atomicMax(&s_maxlen, (int)(p1 - p0));
   __syncthreads();
   const int maxlen = s_maxlen;
-  for (int cs = 0; cs < maxlen; cs += ROWDFT_CHUNK) {
-    const int64_t left = p1 - p0 - cs;
-    const int n = left <= 0 ? 0 : (left < ROWDFT_CHUNK ? (int)left : ROWDFT_CHUNK);
-    __syncthreads();
-    for (int q = tl; q < n; q += tpr) {
-      cols[rl * ROWDFT_CHUNK + q] = __ldg(a.cols + p0 + cs + q);
+  double2* dst[NIN];
 #pragma unroll
-      for (int i = 0; i < NIN; ++i)
-        ws[(i * rpb + rl) * ROWDFT_CHUNK + q] = a.w[i] ? __ldg(a.w[i] + p0 + cs + q) : 1.0;
+  for (int i = 0; i < NIN; ++i) dst[i] = a.out[i] + item * a.out_item + row * a.out_rs;
+#pragma unroll 1
+  for (int pass = 0; pass < npass; ++pass) {
+    const int64_t kb = (int64_t)pass * NF * tpr + tl;  // this thread's frequencies: kb + q * tpr
+    double2 acc[NIN][NF], nyq[NIN];
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) {
+      nyq[i] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) acc[i][q] = make_double2(0.0, 0.0);
     }
-    __syncthreads();
-    for (int p = 0; p < n; ++p) {
-      const int64_t col = cols[rl * ROWDFT_CHUNK + p];
-      double wv[NIN];
+    const bool do_nyq = tl == 0 && pass == 0;
+    for (int cs = 0; cs < maxlen; cs += ROWDFT_CHUNK) {
+      const int64_t left = p1 - p0 - cs;
+      const int n = left <= 0 ? 0 : (left < ROWDFT_CHUNK ? (int)left : ROWDFT_CHUNK);
+      __syncthreads();
+      for (int q = tl; q < n; q += tpr) {
+        cols[rl * ROWDFT_CHUNK + q] = __ldg(a.cols + p0 + cs + q);
 #pragma unroll
-      for (int i = 0; i < NIN; ++i) wv[i] = ws[(i * rpb + rl) * ROWDFT_CHUNK + p];
+        for (int i = 0; i < NIN; ++i)
+          ws[(i * rpb + rl) * ROWDFT_CHUNK + q] = a.w[i] ? __ldg(a.w[i] + p0 + cs + q) : 1.0;
+      }
+      __syncthreads();
+      for (int p = 0; p < n; ++p) {
+        const int64_t col = cols[rl * ROWDFT_CHUNK + p];
+        double wv[NIN];
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) wv[i] = ws[(i * rpb + rl) * ROWDFT_CHUNK + p];
 #if EIK_ROWDFT_SPLIT
-      // W^{col k} = W^{col tl} * W^{col q tpr}: one gathered table read per
-      // point (lane-dependent) and NF row-uniform (broadcast) reads, instead of
-      // NF gathers that touch one cache line per lane
-      const double2 wb = __ldg(a.tw + ((int)((col * tl) & a.last_mask) << a.last_shift));
+        // W^{col k} = W^{col kb} * W^{col q tpr}: one gathered table read per
+        // point (lane-dependent) and NF row-uniform (broadcast) reads, instead of
+        // NF gathers that touch one cache line per lane
+        const double2 wb = __ldg(a.tw + ((int)((col * kb) & a.last_mask) << a.last_shift));
 #endif
 #pragma unroll
-      for (int q = 0; q < NF; ++q) {
+        for (int q = 0; q < NF; ++q) {
 #if EIK_ROWDFT_SPLIT
-        const double2 t = q == 0 ? wb
-                                 : cmul(wb, __ldg(a.tw + ((int)((col * q * tpr) & a.last_mask) << a.last_shift)));
+          const double2 t = q == 0 ? wb
+                                   : cmul(wb, __ldg(a.tw + ((int)((col * q * tpr) & a.last_mask) << a.last_shift)));
 #else
-        const int64_t k = tl + (int64_t)q * tpr;
-        const double2 t = __ldg(a.tw + ((int)((col * k) & a.last_mask) << a.last_shift));
+          const int64_t k = kb + (int64_t)q * tpr;
+          const double2 t = __ldg(a.tw + ((int)((col * k) & a.last_mask) << a.last_shift));
 #endif
 #pragma unroll
-        for (int i = 0; i < NIN; ++i) {
-          acc[i][q].x = fma(wv[i], t.x, acc[i][q].x);
-          acc[i][q].y = fma(wv[i], t.y, acc[i][q].y);
+          for (int i = 0; i < NIN; ++i) {
+            acc[i][q].x = fma(wv[i], t.x, acc[i][q].x);
+            acc[i][q].y = fma(wv[i], t.y, acc[i][q].y);
+          }
         }
-      }
-      if (tl == 0) {
-        const double2 t = __ldg(a.tw + ((int)((col * half) & a.last_mask) << nyq_shift));
+        if (do_nyq) {
+          const double2 t = __ldg(a.tw + ((int)((col * half) & a.last_mask) << nyq_shift));
 #pragma unroll
-        for (int i = 0; i < NIN; ++i) {
-          nyq[i].x = fma(wv[i], t.x, nyq[i].x);
-          nyq[i].y = fma(wv[i], t.y, nyq[i].y);
+          for (int i = 0; i < NIN; ++i) {
+            nyq[i].x = fma(wv[i], t.x, nyq[i].x);
+            nyq[i].y = fma(wv[i], t.y, nyq[i].y);
+          }
         }
       }
     }
-  }
-  if (!valid) return;
+    if (valid) {
 #pragma unroll
-  for (int i = 0; i < NIN; ++i) {
-    double2* dst = a.out[i] + item * a.out_item + row * a.out_rs;
+      for (int i = 0; i < NIN; ++i) {
 #pragma unroll
-    for (int q = 0; q < NF; ++q) dst[(tl + (int64_t)q * tpr) * a.out_ks] = acc[i][q];
-    if (tl == 0) dst[half * a.out_ks] = nyq[i];
+        for (int q = 0; q < NF; ++q) dst[i][(kb + (int64_t)q * tpr) * a.out_ks] = acc[i][q];
+        if (do_nyq) dst[i][half * a.out_ks] = nyq[i];
+      }
+    }
   }
 }
 
@@ -1281,7 +1328,13 @@ inline cudaError_t launch_impulse_rows(const RowDftArgs& ra_in, int n_in, int64_
     ra.out_rs = ra.H;
     ra.out_ks = 1;
   }
-  const int nf = rowdft_nf(ra.H), tpr = rowdft_tpr(ra.H), rpb = ROWDFT_NT / tpr;
+  const int nf = rowdft_nf(ra.H);
+  // transposed layout: EIK_T_NPASS passes so that a CTA holds >= 2 rows (whole sectors per k)
+  ra.npass = 1;
+  if (ra.out_rs == 1)
+    while (ra.npass < EIK_T_NPASS && (ra.H - 1) % (nf * ra.npass * 2) == 0 && (ra.H - 1) / (nf * ra.npass * 2) >= 1)
+      ra.npass *= 2;
+  const int tpr = (int)((ra.H - 1) / (nf * ra.npass)), rpb = ROWDFT_NT / tpr;
   const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
   const dim3 grid((unsigned)((rows + rpb - 1) / rpb), (unsigned)items);
 #define EIK_ROWDFT_NF(NI, F) \

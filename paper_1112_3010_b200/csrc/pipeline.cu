@@ -505,10 +505,12 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
   // Sparse inputs (the BASELINE configs: K << N) go through the row-DFT pass
   // into a dense T[row][k1] and the dense column kernel; EIK_ROWDFT=0 keeps the
   // node-list walk inside the column kernel.
-  static const bool rowdft = [] {
+  // EIK_ROWDFT: 0 = node-list walk for both groups, 2 = for the sign group only
+  static const int rowdft_env = [] {
     const char* e = std::getenv("EIK_ROWDFT");
-    return !(e && e[0] == '0');
+    return e ? e[0] - '0' : 1;
   }();
+  const bool rowdft = rowdft_env == 1 || (rowdft_env == 2 && !sg);
   if (rowdft && p->H <= (int64_t)ROWDFT_NF * ROWDFT_NT) {
     DevBuf& T = sg ? p->tsign : p->trows;
     const int64_t per = (int64_t)p->c[0] * p->H;
