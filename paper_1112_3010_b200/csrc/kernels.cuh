@@ -198,6 +198,7 @@ struct ColArgs {
   const double2* tw;
   int lmax;
   int kfeed;  // set by the launcher: shared-memory feed of register-order kernel spectra
+  int sfeed;  // set by the launcher: asynchronous shared-memory staging of the next dense input (SUM)
   // Peer-block outputs (slab exchange fused into the pass, P2P over NVLink):
   // when blk[0] is set, output row n of component j is written to
   // blk[n >> blk_shift] + j * blk_cstride + item * out_item + (n mod 2^blk_shift) * out_es + l,
@@ -466,6 +467,12 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_KFEED
 #define EIK_KFEED 0
 #endif
+#ifndef EIK_SFEED
+#define EIK_SFEED 0
+#endif
+#ifndef EIK_TWC
+#define EIK_TWC 1
+#endif
 template <int L, int LPCX = 1>
 struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
@@ -481,7 +488,7 @@ struct TmCfg {
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
   // 4096-point lines: the radix-16 NS=256 stage's twiddles W^{t r} are per-thread
   // constants shared by the forward and every inverse -> cached in TMEM too
-  static constexpr bool TWC = (L == 12) && LN::INV_SHARES;
+  static constexpr bool TWC = EIK_TWC && (L == 12) && LN::INV_SHARES;
   static constexpr int WPT_ALL = WPT + (TWC ? 64 : 0);
   static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
@@ -493,7 +500,50 @@ struct TmCfg {
   static constexpr size_t KFEED_BYTES = (size_t)LN::EPT * NT * sizeof(double);
   static constexpr bool KFEED = EIK_KFEED && (SMEM_BYTES + 16 + KFEED_BYTES) * MINB <= 227 * 1024;
   static constexpr size_t SMEM_FEED_BYTES = SMEM_BYTES + (KFEED ? 16 + KFEED_BYTES : 0);
+  // SUM kernels (sign group): the next input line (half-padded: EPT/2 values
+  // per thread, thread-private slots) is staged with cp.async while the
+  // current input is transformed (C2: 64 KB next to 158 KB, one CTA per SM)
+  static constexpr size_t SFEED_BYTES = (size_t)(LN::EPT / 2) * NT * sizeof(double2);
+  static constexpr bool SFEED = EIK_SFEED && (SMEM_BYTES + SFEED_BYTES) * MINB <= 227 * 1024;
+  static constexpr size_t SMEM_SFEED_BYTES = SMEM_BYTES + (SFEED ? SFEED_BYTES : 0);
 };
+
+// cp.async (16-byte, L2 only) global -> shared; src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Stage this thread's non-zero elements of dense input `inp` (half-padded
+// line) into its private slots sbuf[c * NT + tid] without holding registers.
+template <class LN, int NT>
+__device__ __forceinline__ void stage_dense_async(double2* sbuf, const ColArgs& a, int t, int64_t l, int64_t item,
+                                                  int inp, bool valid) {
+  const double2* src = a.din[inp] + item * a.din_item + l * a.din_ls;
+  int c = 0;
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    if (LN::L > 0 && LN::upper_in(r)) continue;
+    const int e = LN::in_idx(t, r);
+    const bool ok = valid && e < a.n_valid;
+    cp_async16(sbuf + c * NT + threadIdx.x, ok ? src + (int64_t)e * a.din_es : a.din[inp], ok ? 16 : 0);
+    ++c;
+  }
+  cp_async_commit();
+}
+template <class LN, int NT>
+__device__ __forceinline__ void unstage_dense(double2 (&v)[LN::EPT], const double2* sbuf) {
+  cp_async_wait_all();
+  int c = 0;
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    if (LN::L > 0 && LN::upper_in(r)) continue;
+    v[r] = sbuf[c * NT + threadIdx.x];
+    ++c;
+  }
+}
 
 template <int L, int IN, int OUT, bool HALF>
 __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpcx(L, OUT)>::MINB)
@@ -533,6 +583,9 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   double2 v[LN::EPT];
   if constexpr (OUT == OUT_SUM) {
     // y = sum_i K_i X_i accumulated in TMEM while each input is transformed in registers
+    constexpr bool SF = TC::SFEED && HALF && IN == IN_DENSE;
+    double2* sbuf = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES);
+    const bool sfeed = SF && a.sfeed;
 #pragma unroll 1
     for (int i = 0; i < a.n_in; ++i) {
 #if EIK_KPF
@@ -543,9 +596,21 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
         kload_all<TC>(kn, a.ks[i], l, t);
       }
 #endif
-      if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
-      else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+      if constexpr (IN == IN_SPARSE) {
+        load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
+      } else if constexpr (SF) {
+        if (sfeed && i > 0) unstage_dense<LN, TC::NT>(v, sbuf);
+        else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+        // the next input lands in this thread's slots while this one is transformed
+        // (input 1 at once; later ones once this input's slots have been read)
+        if (sfeed && i == 0 && a.n_in > 1) stage_dense_async<LN, TC::NT>(sbuf, a, t, l, item, 1, valid);
+      } else {
+        load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+      }
       fft_line<LN, false, HALF>(v, t, xb, tws);
+      if constexpr (SF) {
+        if (sfeed && i >= 1 && i + 1 < a.n_in) stage_dense_async<LN, TC::NT>(sbuf, a, t, l, item, i + 1, valid);
+      }
 #if EIK_KPF
       double kn[LN::EPT];
       if (valid) kload_all<TC>(kn, a.ks[i], l, t);

@@ -16,7 +16,7 @@ template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
   using C = TmCfg<L, tm_lpcx(L, OUT)>;
   auto k = col_tmem_kernel<L, IN, OUT, HALF>;
-  CK(prep_kernel_attr(k, C::SMEM_FEED_BYTES));
+  CK(prep_kernel_attr(k, C::SMEM_FEED_BYTES > C::SMEM_SFEED_BYTES ? C::SMEM_FEED_BYTES : C::SMEM_SFEED_BYTES));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
   if (tiles <= 0 || items <= 0) return EIK_OK;
   if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
@@ -27,7 +27,9 @@ int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
     b.kfeed = 1;
     for (int j = 0; j < a.n_comp; ++j) b.kfeed &= (a.ks[j].perm != nullptr);
   }
-  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, b.kfeed ? C::SMEM_FEED_BYTES : C::SMEM_BYTES, st>>>(b);
+  b.sfeed = (C::SFEED && OUT == OUT_SUM && IN == IN_DENSE && HALF) ? 1 : 0;
+  const size_t smem = b.kfeed ? C::SMEM_FEED_BYTES : b.sfeed ? C::SMEM_SFEED_BYTES : C::SMEM_BYTES;
+  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, smem, st>>>(b);
   CK(cudaGetLastError());
   return EIK_OK;
 }
