@@ -308,6 +308,7 @@ struct TwSrc {
   const double2* q;
   int lq;
   uint32_t tm;  // TMEM address of this thread's cached radix-16 quarter-stage twiddles (0 = none)
+  uint32_t tm2 = 0;  // TMEM address of the last inverse stage's twiddles (radix < 16, NS > 16; 0 = none)
 };
 
 template <class LN, bool INV, int S>
@@ -388,6 +389,15 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
           done = true;
         }
       }
+      if constexpr (INV && S == LN::NST - 1 && S > 0 && LN::st_quarter(INV, S) && R < 16 && R * G == 16) {
+        if (tw.tm2) {  // per-thread constants W^{k r}, group g at R complex slots (slot 0 unused)
+          double2 w[R];
+          tmem_get<R>(tw.tm2 + 4 * R * g, w);
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[g * R + r] = cmulc(v[g * R + r], w[r]);
+          done = true;
+        }
+      }
       if (!done) {
         if constexpr (EIK_TW_POW && LN::TWO_LEVEL && R > 2) {
           // radix <= 8 lines: W^{k r} as powers of W^k (one table lookup per
@@ -430,6 +440,22 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
       for (int r = 0; r < R2; ++r) v[g * R2 + r] = sm[LN::pad(b + r * (LN::M / R2))];
     }
     xb.done();
+  }
+}
+
+// Fill this thread's TMEM copy of the last inverse stage's twiddles (TwSrc::tm2).
+template <class LN>
+__device__ __forceinline__ void tw_last_inv_fill(uint32_t tm2, int t, const double2* q, int lq) {
+  constexpr int S = LN::NST - 1;
+  constexpr int R = LN::rad(true, S), NS = LN::ns(true, S), G = LN::EPT / R;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int k = (t + g * LN::TPL) & (NS - 1);
+    double2 w[R];
+    w[0] = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int r = 1; r < R; ++r) w[r] = twq_get(q, lq, (k * r) << (lq - ilog2c(NS * R)));
+    tmem_put<R>(tm2 + 4 * R * g, w);
   }
 }
 

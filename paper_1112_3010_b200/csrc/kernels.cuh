@@ -473,6 +473,9 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_TWC
 #define EIK_TWC 1
 #endif
+#ifndef EIK_TWI
+#define EIK_TWI 1
+#endif
 template <int L, int LPCX = 1>
 struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
@@ -489,7 +492,16 @@ struct TmCfg {
   // 4096-point lines: the radix-16 NS=256 stage's twiddles W^{t r} are per-thread
   // constants shared by the forward and every inverse -> cached in TMEM too
   static constexpr bool TWC = EIK_TWC && (L == 12) && LN::INV_SHARES;
-  static constexpr int WPT_ALL = WPT + (TWC ? 64 : 0);
+  // other long lines: the last inverse stage (radix R0 < 16 over NS = M/R0 > 16,
+  // quarter-table twiddles otherwise) reads per-thread constants from TMEM
+  // (C5 column kernel 5.19 -> 5.01 ms)
+  static constexpr bool TWI = []() constexpr {
+    if constexpr (F4K) return false;
+    // (radix 2 / 8 groups: one TMEM wait per group costs more than it saves, C3 +2.5%)
+    else return EIK_TWI && LN::EPT == 16 && LN::NST >= 2 && LN::R0 < 16 && LN::R0 >= 4 &&
+                LN::st_quarter(true, LN::NST - 1);
+  }();
+  static constexpr int WPT_ALL = WPT + (TWC ? 64 : 0) + (TWI ? 64 : 0);
   static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
@@ -578,7 +590,12 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     for (int r = 1; r < 16; ++r) w[r] = twq_get(twq, L, t * r);  // W_4096^{t r}, k = t at NS = 256
     tmem_put(ttw, w);
   }
-  const TwSrc tws{sts, twq, L, ttw};
+  uint32_t ttw2 = 0;
+  if constexpr (TC::TWI) {
+    ttw2 = ta + TC::WPT;
+    tw_last_inv_fill<LN>(ttw2, t, twq, L);
+  }
+  const TwSrc tws{sts, twq, L, ttw, ttw2};
 
   double2 v[LN::EPT];
   if constexpr (OUT == OUT_SUM) {
