@@ -13,12 +13,12 @@ lib = sys.argv[1] if len(sys.argv) > 1 else "paper_1112_3010_b200/_lib/libeikfld
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 want = [("col_tmem_kernel<12, 1, 0, true>", r"col_tmem_kernelILi12ELi1ELi0ELb1E"),
         ("col_tmem_kernel<12, 1, 1, true>", r"col_tmem_kernelILi12ELi1ELi1ELb1E"),
-        ("row_kernel<11>", r"row_kernelILi11EE"),
+        ("row_kernel<11, RCP>", r"row_kernelILi11ELb1EE"),
         ("impulse_rows_kernel<1, 8>", r"impulse_rows_kernelILi1ELi8EE"),
         ("col_tmem_kernel<9, 1, 0, true> (C3 axis 0)", r"col_tmem_kernelILi9ELi1ELi0ELb1E"),
         ("lines_kernel<9, true, false> (C3 axis 1 inverse)", r"lines_kernelILi9ELb1ELb0EE"),
         ("col_tmem_kernel<10, 1, 0, true> (C5)", r"col_tmem_kernelILi10ELi1ELi0ELb1E"),
-        ("row_kernel<9> (C5)", r"row_kernelILi9EE")]
+        ("row_kernel<9> (C5)", r"row_kernelILi9ELb0EE")]
 funcs = re.split(r"\n\s*Function : ", sass)
 groups = {"fp64": ("DFMA", "DADD", "DMUL"), "tmem": ("STTM", "LDTM", "UTCATOMSWS", "UTCBAR"),
           "bulk/mbarrier": ("UBLKCP", "SYNCS"), "shared": ("LDS", "STS"), "global": ("LDG", "STG"),
