@@ -532,17 +532,20 @@ __device__ __forceinline__ void f4k_twiddle_row(double2 (&v)[16], int x, const T
   for (int r = 1; r < 16; ++r) v[r] = INV ? cmulc(v[r], row[r]) : cmul(v[r], row[r]);
 }
 
-template <bool HALF_IN>
-__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, double2* sm, const TwSrc& tw) {
+// XB::sync() is the barrier over the threads of this line: the CTA when its
+// lines are interleaved across all warps, a named barrier for line-major CTAs
+template <bool HALF_IN, class XB>
+__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw) {
   constexpr int P = Line4K::PITCH;
+  double2* sm = xb.b0;
   const int g = t >> 4, x = t & 15;
   double2* row = sm + g * P;
   dft<16, false, HALF_IN>(v);  // over n1: v[k1], thread t = n2
   f4k_twiddle_t<false>(v, t, tw);
-  __syncthreads();  // every thread is done with the buffer (previous transform)
+  xb.sync();  // every thread is done with the buffer (previous transform)
 #pragma unroll
   for (int r = 0; r < 16; ++r) sm[r * P + t] = v[r];
-  __syncthreads();
+  xb.sync();
 #pragma unroll
   for (int m = 0; m < 16; ++m) v[m] = row[x + 16 * m];  // row k1 = g, n2 = x + 16 m
   dft<16, false, false>(v);                             // over m: v[a], lane x = j
@@ -556,8 +559,10 @@ __device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, double2* sm
   dft<16, false, false>(v);                             // over j: v[b] = X[g + 16 x + 256 b]
 }
 
-__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, double2* sm, const TwSrc& tw) {
+template <class XB>
+__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw) {
   constexpr int P = Line4K::PITCH;
+  double2* sm = xb.b0;
   const int g = t >> 4, x = t & 15;
   double2* row = sm + g * P;
   dft<16, true, false>(v);  // over b: v[j], lane x = a
@@ -572,10 +577,10 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, double2* sm
   __syncwarp();
 #pragma unroll
   for (int m = 0; m < 16; ++m) row[x + 16 * m] = v[m];
-  __syncthreads();
+  xb.sync();
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = sm[r * P + t];  // thread t = n2: v[k1]
-  __syncthreads();  // buffer free again: the next transform may write any row
+  xb.sync();  // buffer free again: the next transform may write any row
   f4k_twiddle_t<true>(v, t, tw);
   dft<16, true, false>(v);  // over k1: v[i] = x[t + 256 i]
 }
@@ -586,8 +591,8 @@ template <class LN, bool INV, bool HALF_IN = false, class XB>
 __device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw) {
   static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
   if constexpr (LN::FOUR_STEP) {
-    if constexpr (INV) f4k_inverse(v, t, xb.b0, tw);
-    else f4k_forward<HALF_IN>(v, t, xb.b0, tw);
+    if constexpr (INV) f4k_inverse(v, t, xb, tw);
+    else f4k_forward<HALF_IN>(v, t, xb, tw);
   } else {
     stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, tw);
   }

@@ -476,6 +476,9 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_TWI
 #define EIK_TWI 1
 #endif
+#ifndef EIK_F4K_IL
+#define EIK_F4K_IL 2
+#endif
 template <int L, int LPCX = 1>
 struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
@@ -483,7 +486,10 @@ struct TmCfg {
   static constexpr int NT = F4K ? 256 * LPCX : (TPL0 > 256 ? TPL0 : 256);
   static constexpr int LPC = NT / TPL0;
   static constexpr int MINB = NT >= 512 ? 1 : 2;
-  static constexpr int IL = col_il(LPC);
+  // four-step lines: EIK_F4K_IL = 1 makes the CTA line-major (warps 0-7 line 0,
+  // 8-15 line 1) with one named barrier per line, so the lines drift apart and
+  // one line's FP64 phase can overlap the other's exchange
+  static constexpr int IL = F4K ? (EIK_F4K_IL < LPC ? EIK_F4K_IL : LPC) : col_il(LPC);
   using LN = std::conditional_t<F4K, Line4K, PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>;
   using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
