@@ -122,13 +122,29 @@ __host__ __device__ constexpr int row_e(int LH) { return LH >= EIK_ROW_E8_MIN ? 
 #ifndef EIK_ROW_NBUF2_MAX
 #define EIK_ROW_NBUF2_MAX 10
 #endif
+#ifndef EIK_ROW_FEED
+#define EIK_ROW_FEED 1
+#endif
+// rows of >= 64 threads per line get the TMA row feed (C5 512-point rows:
+// 3.69 -> 3.30 ms, trading the ping-pong buffers; C3's 32-thread rows: +12%)
+#ifndef EIK_ROW_FEED_MINTPL
+#define EIK_ROW_FEED_MINTPL 64
+#endif
 template <int LH>
 struct RowCfg {
   using LN = PaddedLine<LH, row_e(LH), row_pad(LH)>;
   static constexpr int NT = (LN::TPL >= 128) ? LN::TPL : 128;
   static constexpr int LPC = NT / LN::TPL;
   static constexpr int TWQ = tpos_size(1 << (LH > 0 ? LH - 1 : 0));  // (2^(LH+1)) / 4, padded
-  static constexpr int NBUF = (LH <= EIK_ROW_NBUF2_MAX && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024) ? 2 : 1;
+  // (with EIK_ROW_FEED_MINTPL < 128, multi-line CTAs give up the ping-pong
+  // buffers for the row feed where both do not fit next to 4 CTAs)
+  static constexpr bool FEED_WANT = EIK_ROW_FEED && LN::TPL >= EIK_ROW_FEED_MINTPL;
+  static constexpr int NBUF = (LH <= EIK_ROW_NBUF2_MAX && (2 * LPC * LN::SMEM + TWQ) * 16 <= 110 * 1024 &&
+                               !(FEED_WANT && LN::TPL < 128 &&
+                                 ((2 * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * 16 + LPC * (LN::M + 1) * 16 + 32) * 4 >
+                                     227 * 1024))
+                                  ? 2
+                                  : 1;
   using XB = XBuf<NBUF, group_sync(1, LPC, LN::TPL), LN::TPL>;  // row kernels are line-major
   static constexpr size_t BASE_BYTES = ((size_t)NBUF * LPC * LN::SMEM + TWQ + LN::ST_SIZE) * sizeof(double2);
   // resident CTAs per SM requested from the register allocator (128 threads:
@@ -144,8 +160,7 @@ struct RowCfg {
 #define EIK_ROW_FEED 1
 #endif
   static constexpr size_t FEED_BYTES = (size_t)LPC * (LN::M + 1) * sizeof(double2) + LPC * sizeof(uint64_t);
-  // (long rows only: measured neutral-to-slower for multi-line CTAs, C3 / C5)
-  static constexpr bool FEED = EIK_ROW_FEED && LN::TPL >= 128 && (BASE_BYTES + FEED_BYTES + 16) * MINB <= 227 * 1024;
+  static constexpr bool FEED = FEED_WANT && (BASE_BYTES + FEED_BYTES + 16) * MINB <= 227 * 1024;
   static constexpr size_t SMEM_BYTES = BASE_BYTES + (FEED ? FEED_BYTES + 16 : 0);
 };
 
