@@ -21,6 +21,8 @@
 // element: every global access is a contiguous run across lines.  Row
 // kernels are line-major (a row is contiguous in memory).
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA stores of the column outputs)
+
 #include "fft_core.cuh"
 #include "tmem.cuh"
 #include "bulk.cuh"
@@ -213,6 +215,8 @@ struct ColArgs {
   const double2* tw;
   int lmax;
   int kfeed;  // set by the launcher: shared-memory feed of register-order kernel spectra
+  int tstore; // set by the launcher: component outputs leave through shared memory + TMA (umap[j])
+  CUtensorMap umap[MAXC];  // [item][row][2 * nlines doubles] view of out[j] (box: 2 LPC doubles x 256 rows)
   int sfeed;  // set by the launcher: asynchronous shared-memory staging of the next dense input (SUM)
   // Peer-block outputs (slab exchange fused into the pass, P2P over NVLink):
   // when blk[0] is set, output row n of component j is written to
@@ -494,6 +498,9 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_F4K_IL
 #define EIK_F4K_IL 2
 #endif
+#ifndef EIK_TSTORE
+#define EIK_TSTORE 0
+#endif
 template <int L, int LPCX = 1>
 struct TmCfg {
   static constexpr int TPL0 = tpl_of(L, 16);
@@ -536,10 +543,58 @@ struct TmCfg {
   // SUM kernels (sign group): the next input line (half-padded: EPT/2 values
   // per thread, thread-private slots) is staged with cp.async while the
   // current input is transformed (C2: 64 KB next to 158 KB, one CTA per SM)
+  // TMA output stores (four-step lines, 2-D distance group): the component's
+  // output tile [M/2 rows][LPC lines] is staged in shared memory and leaves as
+  // 256-row TMA boxes instead of one 16-line global request per warp store
+  static constexpr size_t TSTORE_OFF = (SMEM_BYTES + 127) & ~size_t(127);  // TMA smem boxes: 128-byte aligned
+  static constexpr size_t TSTORE_BYTES = TSTORE_OFF - SMEM_BYTES + (size_t)(LN::M / 2) * LPC * sizeof(double2) + 128;
+  static constexpr bool TSTORE = EIK_TSTORE && F4K && LPC >= 2 && (SMEM_BYTES + TSTORE_BYTES) * MINB <= 227 * 1024;
   static constexpr size_t SFEED_BYTES = (size_t)(LN::EPT / 2) * NT * sizeof(double2);
   static constexpr bool SFEED = EIK_SFEED && (SMEM_BYTES + SFEED_BYTES) * MINB <= 227 * 1024;
   static constexpr size_t SMEM_SFEED_BYTES = SMEM_BYTES + (SFEED ? SFEED_BYTES : 0);
 };
+
+// L2 prefetch for the CTA that runs one resident wave later (linear CTA index
+// + `ahead`, x fastest): its first global reads then hit L2 instead of DRAM.
+#ifndef EIK_L2PF
+#define EIK_L2PF 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool cta_ahead(int ahead, int64_t& bx, int64_t& by) {
+  const int64_t lin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + ahead;
+  bx = lin % gridDim.x;
+  by = lin / gridDim.x;
+  return by < gridDim.y;
+}
+// dense column input of tile (bx, by): rows [0, n_valid) x LPC adjacent lines
+template <int LPC, int NT>
+__device__ __forceinline__ void prefetch_dense_tile(const ColArgs& a, int n_in, int ahead) {
+  int64_t bx, by;
+  if (!cta_ahead(ahead, bx, by)) return;
+  const int64_t l0 = bx * LPC;
+  if (l0 >= a.nlines) return;
+  for (int i = 0; i < n_in; ++i) {
+    const double2* base = a.din[i] + by * a.din_item + l0 * a.din_ls;
+    for (int r = threadIdx.x; r < a.n_valid; r += NT) {
+      const double2* p = base + (int64_t)r * a.din_es;
+      prefetch_l2(p);
+      if (a.din_ls == 1) prefetch_l2(p + LPC - 1);
+    }
+  }
+}
+
+// TMA tensor store (3-D box, shared -> global) and its bulk-group bookkeeping
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 
 // cp.async (16-byte, L2 only) global -> shared; src_bytes = 0 zero-fills
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -599,6 +654,9 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   if (TC::KFEED && a.kfeed && OUT == OUT_COMPS && threadIdx.x == 0) {
     mbar_init(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if constexpr (EIK_L2PF && IN == IN_DENSE) {
+    if (a.din_item > 0 && !a.blk[0]) prefetch_dense_tile<LPC, TC::NT>(a, OUT == OUT_SUM ? a.n_in : 1, 148 * TC::MINB);
   }
   const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle tables
   const uint32_t ta = tmem_thread_addr(tbase, TC::WPT_ALL);
@@ -745,6 +803,47 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   return;
 #endif
 #if EIK_KPF
+  if constexpr (TC::TSTORE && OUT == OUT_COMPS) {
+    if (a.tstore) {
+      // outputs through shared memory and TMA: tile slot (n * LPC + line)
+      // (dynamic shared memory base rounded up to 128 bytes as well)
+      char* sbase = reinterpret_cast<char*>(smem);
+      const uint32_t mis = smem_u32(sbase) & 127u;
+      double2* stg = reinterpret_cast<double2*>(sbase + TC::TSTORE_OFF + (mis ? 128u - mis : 0u));
+      if (valid) kprefetch_all<TC>(a.ks[0], l, t);
+#pragma unroll 1
+      for (int j = 0; j < a.n_comp; ++j) {
+        tmem_get(ta, v);
+        if (valid) {
+          double kn[LN::EPT];
+          kload_all<TC>(kn, a.ks[j], l, t);
+          if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], l, t);
+          kapply_all<LN>(v, kn, a.ks[j], t);
+        }
+        fft_line<LN, true>(v, t, xb, tws);
+        if (j > 0) {  // the previous component's boxes have been read out of the tile
+          if (threadIdx.x == 0) bulk_wait_read0();
+          __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r) {
+          if (LN::L > 0 && LN::upper_in(r)) continue;
+          const int n = LN::in_idx(t, r);
+          if (n < a.n_out) stg[n * LPC + line] = v[r];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          for (int y = 0; y < a.n_out; y += 256)
+            tma_store_3d(&a.umap[j], stg + y * LPC, (int)(blockIdx.x * LPC * 2), y, (int)item);
+          bulk_commit();
+        }
+      }
+      if (threadIdx.x == 0) bulk_wait_read0();
+      tmem_free_cta(tbase, TC::COLS);
+      return;
+    }
+  }
   // kernel spectra: the next component's lines are prefetched into L1 one
   // transform ahead (no registers held across the FFT); loaded at use
   if (valid) kprefetch_all<TC>(a.ks[0], l, t);
@@ -1127,6 +1226,20 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
     }
     __syncwarp();
     feed_issue();
+#if EIK_L2PF
+    // first component's row of the CTA one resident wave later
+    int64_t bx, by;
+    if (t == 0 && a.comp_item > 0 && cta_ahead(148 * RC::MINB, bx, by)) {
+      const int64_t r2 = a.row0 + bx * LPC + line;
+      if (r2 < a.row_end) {
+        const int64_t rb2 = r2 % a.rows_a;
+        const int64_t off2 = (a.item0 + by) * a.comp_item + (r2 / a.rows_a) * a.stride_a +
+                             (rb2 >> a.split_shift) * a.split_stride +
+                             (rb2 & ((int64_t(1) << a.split_shift) - 1)) * a.stride_b;
+        bulk_prefetch_l2(a.comp[0] + off2, ROW_BYTES);
+      }
+    }
+#endif
   }
   // the current component's row: from the prefetch buffer (waits for it) or global
   auto row_src = [&]() -> const double2* {
