@@ -494,13 +494,18 @@ int set_components(const eik_plan* p, bool sign_group, const Roles& r, ColArgs& 
 }
 
 // 2-D: fused column pass of one group straight from the node list.
+// b0 / prep: item-wave mode (items [b0, b0 + B) of a batch whose node CSR was
+// prepared by an earlier call with prep = true over the whole batch)
 int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
-               const Roles& r, double2* const* W, cudaStream_t st) {
+               const Roles& r, double2* const* W, cudaStream_t st, int64_t b0 = 0, bool prep = true) {
   DevBuf& rid = sg ? p->srowid : p->rowid;
   DevBuf& cl = sg ? p->scols : p->cols;
   DevBuf& rp = sg ? p->srowptr : p->rowptr;
-  int rc = prep_nodes(p, nodes, off, K, B, p->N, p->c[0], p->c[1], rid, cl, rp, st, sg ? &p->serr : nullptr);
-  if (rc) return rc;
+  if (prep) {
+    int rc = prep_nodes(p, nodes, off, K, B, p->N, p->c[0], p->c[1], rid, cl, rp, st, sg ? &p->serr : nullptr);
+    if (rc) return rc;
+  }
+  const int64_t* rowptr = rp.as<int64_t>() + b0 * p->c[0];
   const int n_in = sg ? p->dim : 1;
   // Sparse inputs (the BASELINE configs: K << N) go through the row-DFT pass
   // into a dense T[row][k1] and the dense column kernel; EIK_ROWDFT=0 keeps the
@@ -516,7 +521,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     const int64_t per = (int64_t)p->c[0] * p->H;
     CK(T.ensure((size_t)n_in * B * per * sizeof(double2)));
     RowDftArgs ra{};
-    ra.rowptr = rp.as<int64_t>();
+    ra.rowptr = rowptr;
     ra.cols = cl.as<int32_t>();
     ra.n_in = n_in;
     for (int i = 0; i < 3; ++i) {
@@ -552,7 +557,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
               : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st);
   }
   ColArgs a = col_defaults(p);
-  a.rowptr = rp.as<int64_t>();
+  a.rowptr = rowptr;
   a.cols = cl.as<int32_t>();
   a.n_in = sg ? p->dim : 1;
   for (int i = 0; i < 3; ++i) a.w[i] = (sg && i < a.n_in) ? w + (int64_t)i * K : nullptr;
@@ -887,11 +892,30 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
   r.sign = want_sign;
   const int n_comp = r.n_comp();
   const int64_t ce = p->comp_elems();
-  CK(p->comp.ensure((size_t)n_comp * B * ce * sizeof(double2)));
+  // EIK_WAVE=n (2-D distance batches on the row-DFT path): items run in waves
+  // of n, column pass then row pass per wave, so the wave's T and U_j stay in
+  // L2 between the passes instead of round-tripping HBM
+  static const int64_t wave_env = [] {
+    const char* e = std::getenv("EIK_WAVE");
+    return e ? std::atoll(e) : 0;
+  }();
+  static const int rowdft_on = [] {
+    const char* e = std::getenv("EIK_ROWDFT");
+    return e ? e[0] - '0' : 1;
+  }();
+  const bool waves = p->D == 2 && want_phi && !want_sign && wave_env > 0 && B > wave_env && rowdft_on == 1 &&
+                     p->H <= (int64_t)ROWDFT_NF * ROWDFT_NT;
+  const int64_t BW = waves ? wave_env : B;
+  CK(p->comp.ensure((size_t)n_comp * BW * ce * sizeof(double2)));
   std::vector<double2*> W(n_comp);
-  for (int j = 0; j < n_comp; ++j) W[j] = p->comp.as<double2>() + (int64_t)j * B * ce;
+  for (int j = 0; j < n_comp; ++j) W[j] = p->comp.as<double2>() + (int64_t)j * BW * ce;
   int rc;
-  if (p->D == 2) {
+  if (waves) {
+    // node CSR over the whole batch once; the waves index into it
+    if ((rc = prep_nodes(p, d_nodes, d_off, in->n_nodes, B, p->N, p->c[0], p->c[1], p->rowid, p->cols, p->rowptr,
+                         st)))
+      return rc;
+  } else if (p->D == 2) {
     // The two groups are independent column passes: run the sign group on a
     // side stream so it fills the distance group's tail (sequential when
     // profiling, so that per-pass times stay attributable).
@@ -958,6 +982,32 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     CK(cudaStreamWaitEvent(st, p->ev_copies, 0));
     p->copies_pending = false;
   }
+  // the row pass (and, in wave mode, each wave's column pass + row pass)
+  auto finish = [&](const ChunkFn& on_chunk) -> int {
+    if (!waves) return pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark, on_chunk);
+    std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
+    int rc2;
+    if ((rc2 = mark(EIK_PASS_COL, false))) return rc2;
+    for (int64_t b0 = 0; b0 < B; b0 += BW) {
+      const int64_t nb = std::min(BW, B - b0);
+      if ((rc2 = pass_col2d(p, false, d_nodes, d_off, in->n_nodes, nb, nullptr, r, W.data(), st, b0, false)))
+        return rc2;
+      RowArgs rw = ra;
+      const int64_t o = b0 * p->N;
+      auto sh = [o](auto* q) { return q ? q + o : q; };
+      rw.S = sh(rw.S);
+      for (int d = 0; d < 3; ++d) { rw.grad[d] = sh(rw.grad[d]); rw.hess[d] = sh(rw.hess[d]); }
+      rw.mu = sh(rw.mu);
+      rw.mask = sh(rw.mask);
+      rw.uf = sh(rw.uf);
+      rw.phi_out = sh(rw.phi_out);
+      ChunkFn shifted = nullptr;
+      if (on_chunk)
+        shifted = [&, b0](int64_t r0, int64_t r1, int64_t i0, int64_t i1) { return on_chunk(r0, r1, b0 + i0, b0 + i1); };
+      if ((rc2 = pass_finish(p, W.data(), r, p->c[0], p->M[1], nb, rw, st, nomark, shifted))) return rc2;
+    }
+    return mark(EIK_PASS_COL, true);
+  };
   if (host_out && !slots.empty() && !prof && NB >= (int64_t(1) << 22)) {
     // D2H of each finished chunk of rows on a copy stream, overlapping the rest
     // of the row pass (the end-to-end path is PCIe-bound on the outputs)
@@ -984,7 +1034,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
       }
       return EIK_OK;
     };
-    if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark, on_chunk))) return rc;
+    if ((rc = finish(on_chunk))) return rc;
     CK(cudaEventRecord(p->ev_chunk, p->st_copy2));
     CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
     CK(cudaEventRecord(p->ev_copies, p->st_copy));
@@ -992,7 +1042,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     else CK(cudaStreamWaitEvent(st, p->ev_copies, 0));
     slots.clear();
   } else {
-    if ((rc = pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark))) return rc;
+    if ((rc = finish(nullptr))) return rc;
   }
   // ---- copy back / sync / checks
   for (auto& s : slots) CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));

@@ -280,3 +280,41 @@ def test_async_host_runs_match_sync(cuda_ok):
         for a in range(3):
             assert np.array_equal(r["hess"][a], o["hess"][a], equal_nan=True)
     assert _native.ASYNC == 0x40
+
+
+@pytest.mark.parametrize("wave", ["1", "3"])
+def test_item_waves_bit_identical(cuda_ok, wave):
+    """EIK_WAVE=n (batched 2-D distance runs: column pass + row pass per wave
+    of n items) is bit-identical to the whole-batch schedule, for a small
+    ragged batch (one empty item) and a batch large enough for the chunked
+    device-to-host path (whose item ranges the waves shift)."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_1112_3010_b200 import engine
+from paper_1112_3010_b200 import GridSpec
+res = {}
+for tag, counts, ks in (("small", (64, 48), [5, 0, 300, 1, 48, 7, 9]), ("big", (512, 512), [1000] * 20)):
+    grid = GridSpec((0.0, 0.0), 1.0, counts)
+    rng = np.random.default_rng(5)
+    nodes = [np.sort(rng.choice(grid.num_nodes, k, replace=False)) for k in ks]
+    offs = np.cumsum([0] + ks)
+    dt = engine.DistanceTransform(grid, 0.5 if tag == "big" else 1.5, grad=True, hess=tag == "small")
+    o = dt.run_host(np.concatenate(nodes), item_offsets=offs)
+    res[tag + "_S"] = o["S"]
+    res[tag + "_g"] = np.stack(o["grad"])
+    if tag == "small":
+        res[tag + "_h"] = np.stack(o["hess"])
+    res[tag + "_uf"] = o["underflow"]
+np.savez(sys.argv[1], **res)
+''' % REPO
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        outs = []
+        for i, e in enumerate(({"EIK_WAVE": "0"}, {"EIK_WAVE": wave})):
+            f = os.path.join(d, f"o{i}.npz")
+            subprocess.run([sys.executable, "-c", code, f], check=True, env={**os.environ, **e})
+            outs.append(np.load(f))
+        for k in outs[0].files:
+            assert np.array_equal(outs[0][k], outs[1][k], equal_nan=True), k
