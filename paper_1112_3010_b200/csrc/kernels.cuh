@@ -1278,7 +1278,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   };
   auto active = [&](int r) { return !(LN::L > 0 && LN::upper_in(r)); };
 
-  double2 phi[E], sg[3][E];
+  double2 phi[E], sg[2][E];
   double2 z[E];
   // RCP: after the S epilogue phi[] holds scale / phi (one division per node
   // instead of one per component, no extra registers; <= 1.5 ulp instead of
@@ -1327,12 +1327,16 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
       for (int r = 0; r < E; ++r) {
         if (!active(r)) continue;
         const double2 q = ratio(z[r], r);
-        if (d == 0) sg[0][r] = q; else if (d == 1) sg[1][r] = q; else sg[2][r] = q;
+        // kept for the Hessian epilogue only (RCP <=> Hessian plan, 2-D): the
+        // gradient-only instantiations hold no ratios across components
+        if constexpr (RCP) {
+          if (d == 0) sg[0][r] = q; else sg[1][r] = q;
+        }
         if (a.grad[d]) put(a.grad[d], r, q.x, q.y);
       }
     }
   }
-  if (a.c_hess >= 0) {
+  if (RCP && a.c_hess >= 0) {
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
       row_c2r(a.comp[a.c_hess + d] + roff);
