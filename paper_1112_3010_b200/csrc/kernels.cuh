@@ -1573,11 +1573,12 @@ inline cudaError_t launch_impulse_rows(const RowDftArgs& ra_in, int n_in, int64_
 // ---------------------------------------------------------------------------
 // Node-list preparation: validation + per-row CSR, deterministic.
 
+// item_off == nullptr: one item holding all K nodes (no offsets array to upload)
 static __global__ void prep_nodes_kernel(const int64_t* __restrict__ nodes, const int64_t* __restrict__ item_off,
-                                  int64_t clast, int64_t rows_per_item, int64_t N,
+                                  int64_t K, int64_t clast, int64_t rows_per_item, int64_t N,
                                   int64_t* __restrict__ rowid, int32_t* __restrict__ cols, int* err) {
   const int64_t item = blockIdx.y;
-  const int64_t p0 = item_off[item], p1 = item_off[item + 1];
+  const int64_t p0 = item_off ? item_off[item] : 0, p1 = item_off ? item_off[item + 1] : K;
   for (int64_t p = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t nd = nodes[p];
     if (nd < 0 || nd >= N || (p > p0 && nodes[p - 1] >= nd)) atomicExch(err, 1);

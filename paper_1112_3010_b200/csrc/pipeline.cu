@@ -120,7 +120,7 @@ struct eik_plan {
   std::vector<std::unique_ptr<KDev>> ksign;
   std::vector<std::unique_ptr<KDev>> ksweep;  // tau sweep: one exp kernel per tau
   std::vector<double> taus;
-  DevBuf comp, vin, rowid, cols, rowptr, srowid, scols, srowptr, off1, soff;
+  DevBuf comp, vin, rowid, cols, rowptr, srowid, scols, srowptr;
   DevBuf h_nodes, h_off, h_snodes, h_sw, stage, counter, err, work;
   std::mutex mu;
   cudaEvent_t ev[2 * EIK_NPASS] = {};
@@ -337,7 +337,7 @@ int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_
   if (K > 0) {
     const int64_t per = std::max<int64_t>(1, std::min<int64_t>(1024, (K / std::max<int64_t>(items, 1) + 255) / 256));
     prep_nodes_kernel<<<dim3((unsigned)per, (unsigned)items), 256, 0, st>>>(
-        d_nodes, d_off, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), err.as<int>());
+        d_nodes, d_off, K, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), err.as<int>());
     CK(cudaGetLastError());
   }
   rowptr_kernel<<<(unsigned)((nrows + 1 + 255) / 256), 256, 0, st>>>(rowid.as<int64_t>(), K, nrows,
@@ -416,7 +416,6 @@ int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double 
     p->work.release();
   }
   CK(p->counter.ensure(sizeof(unsigned long long)));
-  CK(p->off1.ensure(2 * sizeof(int64_t)));
   *out = p.release();
   return EIK_OK;
 }
@@ -836,11 +835,9 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
       d_off = p->h_off.as<int64_t>();
     }
   }
-  if (want_phi && B == 1 && (!d_off || host_in)) {
-    const int64_t off[2] = {0, in->n_nodes};
-    CK(cudaMemcpyAsync(p->off1.p, off, sizeof(off), cudaMemcpyHostToDevice, st));
-    d_off = p->off1.as<int64_t>();
-  }
+  // one item: prep_nodes takes [0, n_nodes) without an offsets array (no
+  // pageable 16-byte upload on the stream)
+  if (want_phi && B == 1 && (!d_off || host_in)) d_off = nullptr;
   if (want_sign) {
     if (host_in) {
       CK(p->h_snodes.ensure(Ks * sizeof(int64_t)));
@@ -850,9 +847,6 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
       d_snodes = p->h_snodes.as<int64_t>();
       d_sw = p->h_sw.as<double>();
     }
-    CK(p->soff.ensure(2 * sizeof(int64_t)));
-    const int64_t off[2] = {0, Ks};
-    CK(cudaMemcpyAsync(p->soff.p, off, sizeof(off), cudaMemcpyHostToDevice, st));
   }
   // ---- outputs (device pointers, possibly staged)
   const int64_t NB = p->N * B;
@@ -931,7 +925,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     }
     if (want_sign) {
       if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
-      if ((rc = pass_col2d(p, true, d_snodes, p->soff.as<int64_t>(), Ks, 1, d_sw, r, W.data(), ss))) return rc;
+      if ((rc = pass_col2d(p, true, d_snodes, nullptr, Ks, 1, d_sw, r, W.data(), ss))) return rc;
       if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
     }
     if (fork) CK(cudaEventRecord(p->ev_join, ss));
@@ -954,7 +948,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     }
     if (want_sign) {
       if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
-      if ((rc = pass_planes(p, true, d_snodes, p->soff.as<int64_t>(), Ks, 1, d_sw, p->c[0], p->M[1], V, st)))
+      if ((rc = pass_planes(p, true, d_snodes, nullptr, Ks, 1, d_sw, p->c[0], p->M[1], V, st)))
         return rc;
       if ((rc = pass_axis0(p, true, V, 0, p->M[1], 1, r, W.data(), st))) return rc;
       if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
@@ -1170,16 +1164,12 @@ int eik_slab_planes(eik_plan* p, int group, const int64_t* nodes, int64_t n_node
   if (group == 0 && !r.phi) return fail(EIK_EVALIDATION, "plan was built without the distance kernels");
   if (ks < 1 || p->M[1] % ks || (ks & (ks - 1)) || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DevBuf& off = group ? p->soff : p->off1;
-  CK(off.ensure(2 * sizeof(int64_t)));
-  const int64_t o[2] = {0, n_nodes};
-  CK(cudaMemcpyAsync(off.p, o, sizeof(o), cudaMemcpyHostToDevice, st));
   double2* V[3] = {nullptr, nullptr, nullptr};
   if (!p2p) {
     V[0] = (double2*)v_out[0];
     if (group) { V[1] = (double2*)v_out[1]; V[2] = (double2*)v_out[2]; }
   }
-  if ((rc = pass_planes(p, group == 1, nodes, off.as<int64_t>(), n_nodes, 1, weights, c0_local, ks, V, st,
+  if ((rc = pass_planes(p, group == 1, nodes, nullptr, n_nodes, 1, weights, c0_local, ks, V, st,
                         p2p ? &pb : nullptr)))
     return rc;
   if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
@@ -1276,7 +1266,6 @@ int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const 
   CK(cudaDeviceSynchronize());
   p->work.release();
   CK(p->counter.ensure(sizeof(unsigned long long)));
-  CK(p->off1.ensure(2 * sizeof(int64_t)));
   *out = p.release();
   return EIK_OK;
 }
@@ -1296,8 +1285,6 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
     CK(cudaMemcpyAsync(p->h_nodes.p, nodes, n_nodes * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     d_nodes = p->h_nodes.as<int64_t>();
   }
-  const int64_t off[2] = {0, n_nodes};
-  CK(cudaMemcpyAsync(p->off1.p, off, sizeof(off), cudaMemcpyHostToDevice, st));
   std::vector<double*> outs(S, S + nt);
   if (host_out) {
     CK(p->stage.ensure((size_t)nt * p->N * sizeof(double)));
@@ -1307,7 +1294,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
   CK(p->comp.ensure((size_t)std::min(nt, MAXC) * ce * sizeof(double2)));
   CK(p->counter.ensure(sizeof(unsigned long long)));
   CK(cudaMemsetAsync(p->counter.p, 0, sizeof(unsigned long long), st));
-  int rc = prep_nodes(p, d_nodes, p->off1.as<int64_t>(), n_nodes, 1, p->N, p->c[0], p->c[1], p->rowid, p->cols,
+  int rc = prep_nodes(p, d_nodes, nullptr, n_nodes, 1, p->N, p->c[0], p->c[1], p->rowid, p->cols,
                       p->rowptr, st);
   if (rc) return rc;
   // impulse DFT once; every chunk of <= 8 taus reuses T
