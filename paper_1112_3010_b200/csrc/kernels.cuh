@@ -1573,30 +1573,70 @@ inline cudaError_t launch_impulse_rows(const RowDftArgs& ra_in, int n_in, int64_
 // ---------------------------------------------------------------------------
 // Node-list preparation: validation + per-row CSR, deterministic.
 
-// item_off == nullptr: one item holding all K nodes (no offsets array to upload)
-static __global__ void prep_nodes_kernel(const int64_t* __restrict__ nodes, const int64_t* __restrict__ item_off,
-                                  int64_t K, int64_t clast, int64_t rows_per_item, int64_t N,
-                                  int64_t* __restrict__ rowid, int32_t* __restrict__ cols, int* err) {
+// item_off == nullptr: one item holding all K nodes (no offsets array to upload).
+// Also builds the per-row CSR rowptr[r] = first node p with rowid[p] >= r
+// (rows_per_item * items + 1 entries), each entry written exactly once for a
+// sorted node list: node p writes the rows after its predecessor's row up to
+// its own; the item's last node fills the rows after it; an empty item fills
+// all of its rows.  Gaps of 32+ rows are written by the whole warp.  (Unsorted
+// lists set *err and may leave rows unwritten; the buffer is zeroed at
+// allocation, so stale entries stay inside the node range.)
+static __global__ void __launch_bounds__(256) prep_nodes_kernel(const int64_t* __restrict__ nodes,
+                                                                const int64_t* __restrict__ item_off, int64_t K,
+                                                                int64_t clast, int64_t rows_per_item, int64_t N,
+                                                                int64_t* __restrict__ rowid, int32_t* __restrict__ cols,
+                                                                int64_t* __restrict__ rowptr, int* err) {
   const int64_t item = blockIdx.y;
   const int64_t p0 = item_off ? item_off[item] : 0, p1 = item_off ? item_off[item + 1] : K;
-  for (int64_t p = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t nd = nodes[p];
-    if (nd < 0 || nd >= N || (p > p0 && nodes[p - 1] >= nd)) atomicExch(err, 1);
-    const int64_t ndc = nd < 0 ? 0 : (nd >= N ? N - 1 : nd);
-    rowid[p] = item * rows_per_item + ndc / clast;
-    cols[p] = (int32_t)(ndc % clast);
+  const int64_t rbase = item * rows_per_item, rend = rbase + rows_per_item;  // this item's rows [rbase, rend)
+  const bool last_item = item + 1 == (int64_t)gridDim.y;
+  if (p0 >= p1) {  // empty item
+    if (blockIdx.x == 0) {
+      for (int64_t r = rbase + threadIdx.x; r < rend; r += blockDim.x) rowptr[r] = p0;
+      if (last_item && threadIdx.x == 0) rowptr[rend] = p1;
+    }
+    return;
   }
-}
-
-static __global__ void rowptr_kernel(const int64_t* __restrict__ rowid, int64_t K, int64_t nrows, int64_t* __restrict__ rowptr) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r > nrows) return;
-  int64_t lo = 0, hi = K;  // first p with rowid[p] >= r
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (rowid[mid] < r) lo = mid + 1; else hi = mid;
+  const int lane = threadIdx.x & 31;
+  auto row_of = [&](int64_t nd) { return rbase + (nd < 0 ? 0 : (nd >= N ? N - 1 : nd)) / clast; };
+  // rows [lo, hi] get value v: short runs by the thread, long ones by the warp
+  auto fill = [&](int64_t lo, int64_t hi, int64_t v) {
+    const bool lng = hi - lo >= 32;
+    if (!lng)
+      for (int64_t r = lo; r <= hi; ++r) rowptr[r] = v;
+    unsigned m = __ballot_sync(0xffffffffu, lng);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t lj = __shfl_sync(0xffffffffu, lo, j), hj = __shfl_sync(0xffffffffu, hi, j);
+      const int64_t vj = __shfl_sync(0xffffffffu, v, j);
+      for (int64_t r = lj + lane; r <= hj; r += 32) rowptr[r] = vj;
+    }
+  };
+  // warp-uniform trip count (p = pw + lane)
+  for (int64_t pw = p0 + blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); pw < p1;
+       pw += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = pw + lane;
+    int64_t lo = 0, hi = -1, tlo = 0, thi = -1;
+    if (p < p1) {
+      const int64_t nd = nodes[p];
+      const int64_t prev = p > p0 ? nodes[p - 1] : -1;
+      if (nd < 0 || nd >= N || (p > p0 && prev >= nd)) atomicExch(err, 1);
+      const int64_t ndc = nd < 0 ? 0 : (nd >= N ? N - 1 : nd);
+      const int64_t rr = rbase + ndc / clast;
+      rowid[p] = rr;
+      cols[p] = (int32_t)(ndc % clast);
+      lo = p > p0 ? row_of(prev) + 1 : rbase;
+      hi = rr;
+      if (p + 1 == p1) {  // rows after the item's last node
+        tlo = rr + 1;
+        thi = rend - 1;
+        if (last_item) rowptr[rend] = p1;
+      }
+    }
+    fill(lo, hi, p);
+    fill(tlo, thi, p1);
   }
-  rowptr[r] = lo;
 }
 
 }  // namespace eik

@@ -331,17 +331,16 @@ int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_
   DevBuf& err = errbuf ? *errbuf : p->err;
   CK(rowid.ensure(std::max<int64_t>(K, 1) * sizeof(int64_t)));
   CK(cols.ensure(std::max<int64_t>(K, 1) * sizeof(int32_t)));
+  const void* rp_old = rowptr.p;
   CK(rowptr.ensure((nrows + 1) * sizeof(int64_t)));
+  if (rowptr.p != rp_old) CK(cudaMemsetAsync(rowptr.p, 0, rowptr.bytes, st));
   CK(err.ensure(sizeof(int)));
   CK(cudaMemsetAsync(err.p, 0, sizeof(int), st));
-  if (K > 0) {
-    const int64_t per = std::max<int64_t>(1, std::min<int64_t>(1024, (K / std::max<int64_t>(items, 1) + 255) / 256));
-    prep_nodes_kernel<<<dim3((unsigned)per, (unsigned)items), 256, 0, st>>>(
-        d_nodes, d_off, K, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), err.as<int>());
-    CK(cudaGetLastError());
-  }
-  rowptr_kernel<<<(unsigned)((nrows + 1 + 255) / 256), 256, 0, st>>>(rowid.as<int64_t>(), K, nrows,
-                                                                       rowptr.as<int64_t>());
+  // node validation, row ids / columns and the row CSR in one launch
+  const int64_t per = std::max<int64_t>(1, std::min<int64_t>(1024, (K / std::max<int64_t>(items, 1) + 255) / 256));
+  prep_nodes_kernel<<<dim3((unsigned)per, (unsigned)items), 256, 0, st>>>(
+      d_nodes, d_off, K, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), rowptr.as<int64_t>(),
+      err.as<int>());
   CK(cudaGetLastError());
   return EIK_OK;
 }
