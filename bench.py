@@ -84,6 +84,9 @@ def build_workload(cfg, seed, rank=0, world=1, items=512):
     raise ValueError(cfg)
 
 
+SURVEY_BYTES_PER_POINT = {"C1": 264, "C2": 696, "C3": 768, "C4": 1640, "C5": 264}
+
+
 def algorithmic_bytes(plan_info, w, batch):
     """Compulsory HBM bytes per launch of each pass (DESIGN.md §Roofline model).
 
@@ -460,6 +463,15 @@ def main():
                 "peak_nominal": 8000.0, "frac_nominal": round(ach / 8000.0, 4),
                 "step_bytes": sum(alg.values()),
                 "step_frac": round(sum(alg.values()) / (total_ms / a.steps / 1e3) / 1e9 / peak, 4)}
+        # SURVEY.md 8(d)'s looser "pruned, fused, out-of-core pass model" (B per
+        # grid point: forward + inverse passes that each round-trip HBM), for
+        # comparison with the survey's ideal Gpts/s; the tighter model above is
+        # the one `frac` / `step_frac` use
+        bpp = SURVEY_BYTES_PER_POINT.get(a.config)
+        if bpp:
+            sb = bpp * w["grid"].num_nodes * B
+            roof["survey_pass_model"] = {"bytes_per_point": bpp, "step_bytes": sb,
+                                         "step_frac": round(sb / (total_ms / a.steps / 1e3) / 1e9 / peak, 4)}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

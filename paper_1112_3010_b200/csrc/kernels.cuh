@@ -361,6 +361,20 @@ __device__ __forceinline__ void load_dense(double2 (&v)[LN::EPT], const ColArgs&
   }
 }
 
+// L2 prefetch of this thread's part of a dense input line (no registers held)
+template <class LN, bool HALF>
+__device__ __forceinline__ void prefetch_dense_l2(const ColArgs& a, int t, int64_t l, int64_t item, int inp,
+                                                  bool valid) {
+  if (!valid) return;
+  const double2* __restrict__ src = a.din[inp] + item * a.din_item + l * a.din_ls;
+#pragma unroll
+  for (int r = 0; r < LN::EPT; ++r) {
+    if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
+    const int e = LN::in_idx(t, r);
+    if (e < a.n_valid) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + (int64_t)e * a.din_es));
+  }
+}
+
 // Fused axis-0 column kernel.  blockIdx.x: tile of LPC lines, blockIdx.y: item.
 template <int L, int IN, int OUT, bool HALF>
 __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constant__ ColArgs a) {
@@ -488,6 +502,9 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #endif
 #ifndef EIK_SFEED
 #define EIK_SFEED 0
+#endif
+#ifndef EIK_SPF
+#define EIK_SPF 1
 #endif
 #ifndef EIK_TWC
 #define EIK_TWC 1
@@ -702,6 +719,8 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
         if (sfeed && i == 0 && a.n_in > 1) stage_dense_async<LN, TC::NT>(sbuf, a, t, l, item, 1, valid);
       } else {
         load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+        // the next input's line heads for L2 while this one is transformed
+        if (EIK_SPF && i + 1 < a.n_in) prefetch_dense_l2<LN, HALF>(a, t, l, item, i + 1, valid);
       }
       fft_line<LN, false, HALF>(v, t, xb, tws);
       if constexpr (SF) {
