@@ -1598,13 +1598,13 @@ inline cudaError_t launch_impulse_rows(const RowDftArgs& ra_in, int n_in, int64_
 // sorted node list: node p writes the rows after its predecessor's row up to
 // its own; the item's last node fills the rows after it; an empty item fills
 // all of its rows.  Gaps of 32+ rows are written by the whole warp.  (Unsorted
-// lists set *err and may leave rows unwritten; the buffer is zeroed at
+// lists set *err = gen (the caller's run generation) and may leave rows unwritten; the buffer is zeroed at
 // allocation, so stale entries stay inside the node range.)
 static __global__ void __launch_bounds__(256) prep_nodes_kernel(const int64_t* __restrict__ nodes,
                                                                 const int64_t* __restrict__ item_off, int64_t K,
                                                                 int64_t clast, int64_t rows_per_item, int64_t N,
                                                                 int64_t* __restrict__ rowid, int32_t* __restrict__ cols,
-                                                                int64_t* __restrict__ rowptr, int* err) {
+                                                                int64_t* __restrict__ rowptr, int* err, int gen) {
   const int64_t item = blockIdx.y;
   const int64_t p0 = item_off ? item_off[item] : 0, p1 = item_off ? item_off[item + 1] : K;
   const int64_t rbase = item * rows_per_item, rend = rbase + rows_per_item;  // this item's rows [rbase, rend)
@@ -1640,7 +1640,7 @@ static __global__ void __launch_bounds__(256) prep_nodes_kernel(const int64_t* _
     if (p < p1) {
       const int64_t nd = nodes[p];
       const int64_t prev = p > p0 ? nodes[p - 1] : -1;
-      if (nd < 0 || nd >= N || (p > p0 && prev >= nd)) atomicExch(err, 1);
+      if (nd < 0 || nd >= N || (p > p0 && prev >= nd)) atomicExch(err, gen);
       const int64_t ndc = nd < 0 ? 0 : (nd >= N ? N - 1 : nd);
       const int64_t rr = rbase + ndc / clast;
       rowid[p] = rr;

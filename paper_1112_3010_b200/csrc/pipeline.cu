@@ -3,6 +3,7 @@
 // extern "C" entry points declared in include/eikfld_b200.h.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -123,6 +124,9 @@ struct eik_plan {
   DevBuf comp, vin, rowid, cols, rowptr, srowid, scols, srowptr;
   DevBuf h_nodes, h_off, h_snodes, h_sw, stage, counter, err, work;
   std::mutex mu;
+  // run generation: prep_nodes marks an invalid node list by writing the
+  // current generation into err / serr, so the flags need no reset per run
+  int run_gen = 0;
   cudaEvent_t ev[2 * EIK_NPASS] = {};
   bool ev_used[EIK_NPASS] = {};
   // side stream: the 2-D sign group runs concurrently with the distance group
@@ -334,13 +338,14 @@ int prep_nodes(eik_plan* p, const int64_t* d_nodes, const int64_t* d_off, int64_
   const void* rp_old = rowptr.p;
   CK(rowptr.ensure((nrows + 1) * sizeof(int64_t)));
   if (rowptr.p != rp_old) CK(cudaMemsetAsync(rowptr.p, 0, rowptr.bytes, st));
+  const void* err_old = err.p;
   CK(err.ensure(sizeof(int)));
-  CK(cudaMemsetAsync(err.p, 0, sizeof(int), st));
+  if (err.p != err_old) CK(cudaMemsetAsync(err.p, 0, sizeof(int), st));
   // node validation, row ids / columns and the row CSR in one launch
   const int64_t per = std::max<int64_t>(1, std::min<int64_t>(1024, (K / std::max<int64_t>(items, 1) + 255) / 256));
   prep_nodes_kernel<<<dim3((unsigned)per, (unsigned)items), 256, 0, st>>>(
       d_nodes, d_off, K, clast, rows_per_item, N_item, rowid.as<int64_t>(), cols.as<int32_t>(), rowptr.as<int64_t>(),
-      err.as<int>());
+      err.as<int>(), p->run_gen);
   CK(cudaGetLastError());
   return EIK_OK;
 }
@@ -790,6 +795,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
   if (!p || !in || !out) return fail(EIK_EVALIDATION, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   CK(cudaSetDevice(p->device));
+  p->run_gen = p->run_gen == INT_MAX ? 1 : p->run_gen + 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t B = in->batch < 1 ? 1 : in->batch;
   const bool host_in = flags & EIK_HOST_INPUTS, host_out = flags & EIK_HOST_OUTPUTS;
@@ -1051,7 +1057,8 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     }
     if (count) CK(cudaMemcpyAsync(&nuf, ctr, sizeof(nuf), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (err_flag || serr_flag) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
+    if (err_flag == p->run_gen || serr_flag == p->run_gen)
+      return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
     if (out->n_underflow) *out->n_underflow = (int64_t)nuf;
     if ((flags & EIK_CHECK_UNDERFLOW) && nuf > 0)
       return fail(EIK_EUNDERFLOW, "phi has non-positive entries after convolution; increase the precision bits "
@@ -1275,6 +1282,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
   if (p->ksweep.empty()) return fail(EIK_EVALIDATION, "plan was not built for a tau sweep");
   std::lock_guard<std::mutex> lock(p->mu);
   CK(cudaSetDevice(p->device));
+  p->run_gen = p->run_gen == INT_MAX ? 1 : p->run_gen + 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool host_in = flags & EIK_HOST_INPUTS, host_out = flags & EIK_HOST_OUTPUTS;
   const int nt = (int)p->taus.size();
@@ -1363,7 +1371,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
     CK(cudaMemcpyAsync(&err_flag, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&nuf, p->counter.p, sizeof(nuf), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (err_flag) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
+    if (err_flag == p->run_gen) return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
     if (n_underflow) *n_underflow = (int64_t)nuf;
     if ((flags & EIK_CHECK_UNDERFLOW) && nuf > 0)
       return fail(EIK_EUNDERFLOW, "phi has non-positive entries after convolution; increase the precision bits "

@@ -86,6 +86,19 @@ def test_invalid_inputs_rejected(cuda_ok):
     bad = PointSet(points=np.zeros((1, 2)), snapped_indices=np.array([300]))
     with pytest.raises(ValidationError):
         distance.s_fft(bad, grid, PrecisionConfig.native64(1.0))
+    # the invalid-node flag belongs to its own run: valid / invalid / valid /
+    # unsorted runs back to back on one plan (the flag is never reset on the
+    # device, each run compares it with its own generation)
+    good = np.array([5, 77, 200], dtype=np.int64)
+    ref = np.empty(256)
+    plan.run(good, S=ref, count=True)
+    with pytest.raises(ValidationError):
+        plan.run(np.array([9, 9], dtype=np.int64), S=np.empty(256), count=True)
+    again = np.empty(256)
+    plan.run(good, S=again, count=True)
+    assert np.array_equal(ref, again)
+    with pytest.raises(ValidationError):
+        plan.run(np.array([200, 5], dtype=np.int64), S=np.empty(256), count=True)  # unsorted
 
 
 @pytest.mark.parametrize("env,exact", [({"EIK_ROWDFT": "0"}, False), ({"EIK_TMEM": "0"}, False),
