@@ -1449,6 +1449,12 @@ constexpr int ROWDFT_NT = 256;
 #ifndef EIK_T_NPASS
 #define EIK_T_NPASS 2
 #endif
+#ifndef EIK_T_NPASS_RM
+#define EIK_T_NPASS_RM 4
+#endif
+#ifndef EIK_T_MINCTA
+#define EIK_T_MINCTA (148 * 16)
+#endif
 #ifndef EIK_ROWDFT_SPLIT
 #define EIK_ROWDFT_SPLIT 1
 #endif
@@ -1569,10 +1575,19 @@ inline cudaError_t launch_impulse_rows(const RowDftArgs& ra_in, int n_in, int64_
   }
   const int nf = rowdft_nf(ra.H);
   // transposed layout: EIK_T_NPASS passes so that a CTA holds >= 2 rows (whole sectors per k)
+  // (row-major layout: up to EIK_T_NPASS_RM passes, i.e. that many times more
+  // rows per CTA, whose node lists are staged together, while the launch keeps
+  // >= EIK_T_MINCTA CTAs: C5 impulse rows -2.3% of its column pass at 4 passes;
+  // C2 with 2048 rows keeps one row per CTA, 4 rows per CTA cost it +8%)
   ra.npass = 1;
-  if (ra.out_rs == 1)
-    while (ra.npass < EIK_T_NPASS && (ra.H - 1) % (nf * ra.npass * 2) == 0 && (ra.H - 1) / (nf * ra.npass * 2) >= 1)
-      ra.npass *= 2;
+  const int want = ra.out_rs == 1 ? EIK_T_NPASS : EIK_T_NPASS_RM;
+  auto ctas = [&](int np) {
+    const int64_t rp = ROWDFT_NT / ((ra.H - 1) / (nf * np));
+    return (rows + rp - 1) / rp * items;
+  };
+  while (ra.npass < want && (ra.H - 1) % (nf * ra.npass * 2) == 0 && (ra.H - 1) / (nf * ra.npass * 2) >= 1 &&
+         (ra.out_rs == 1 || ctas(ra.npass * 2) >= EIK_T_MINCTA))
+    ra.npass *= 2;
   const int tpr = (int)((ra.H - 1) / (nf * ra.npass)), rpb = ROWDFT_NT / tpr;
   const size_t smem = (size_t)rpb * (ROWDFT_STAGE / rpb) * (n_in * sizeof(double) + sizeof(int32_t));
   const dim3 grid((unsigned)((rows + rpb - 1) / rpb), (unsigned)items);
