@@ -243,6 +243,40 @@ def test_ragged_batch_with_empty_item(cuda_ok):
     assert batch["n_underflow"] == int(batch["underflow"].sum())
 
 
+@pytest.mark.parametrize("counts", [(40, 72), (12, 10, 20)])
+def test_batch_row_csr_gaps(cuda_ok, counts):
+    """Row CSR built by prep_nodes: empty first and last items, items whose
+    only nodes sit in their first or last row (long leading / trailing gaps,
+    filled warp-cooperatively), and a dense item; every item equals its own
+    single run bit for bit (2-D and 3-D)."""
+    from paper_1112_3010_b200 import engine
+
+    grid = _grid(counts)
+    N = grid.num_nodes
+    last = counts[-1]
+    rng = rng_for(91)
+    items = [
+        np.array([], dtype=np.int64),
+        np.array([0], dtype=np.int64),                      # first row only
+        np.array([N - 1], dtype=np.int64),                  # last row only
+        np.array([N // 2 - 3, N // 2 + last], dtype=np.int64),
+        np.sort(rng.choice(N, N // 3, replace=False)),       # dense
+        np.array([], dtype=np.int64),
+    ]
+    offs = np.cumsum([0] + [len(x) for x in items])
+    dt = engine.DistanceTransform(grid, 1.5, grad=True)
+    batch = dt.run_host(np.concatenate(items), item_offsets=offs)
+    for i, nd in enumerate(items):
+        sl = slice(i * N, (i + 1) * N)
+        if not len(nd):
+            assert np.isnan(batch["S"][sl]).all()
+            continue
+        single = dt.run_host(nd)
+        assert np.array_equal(single["S"], batch["S"][sl], equal_nan=True), i
+        for a in range(len(counts)):
+            assert np.array_equal(single["grad"][a], batch["grad"][a][sl], equal_nan=True), i
+
+
 def test_duplicate_points_collapse(cuda_ok):
     """Duplicated (and unsnapped) points collapse to one unit impulse per
     node, as PointSet.distinct_nodes does in the reference (R/grid.py:89-121)."""
