@@ -3,6 +3,7 @@
 // extern "C" entry points declared in include/eikfld_b200.h.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -33,6 +34,10 @@ int eik_fail(int code, const std::string& msg) {
 }
 
 namespace {
+// bumped on every device allocation of a DevBuf: a captured CUDA graph is
+// replayed only while no plan buffer it references can have moved
+std::atomic<uint64_t> g_alloc_epoch{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -50,6 +55,7 @@ struct DevBuf {
     release();
     cudaError_t e = cudaMalloc(&p, b ? b : 16);
     if (e == cudaSuccess) bytes = b ? b : 16;
+    g_alloc_epoch.fetch_add(1);
     return e;
   }
   template <class T>
@@ -141,7 +147,16 @@ struct eik_plan {
   int64_t p2p_c0loc = 0, p2p_ks = 0, p2p_slot = 0;  // complex elements per slot
   std::vector<double2*> p2p_peer;
   std::vector<void*> p2p_opened;
+  // CUDA graph of a repeated device-resident eik_run (see eik_run)
+  cudaStream_t st_cap = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool gkey_valid = false, seen_valid = false;
+  unsigned char gkey[sizeof(eik_inputs) + sizeof(eik_outputs) + sizeof(uint32_t)] = {};
+  unsigned char seen[sizeof(eik_inputs) + sizeof(eik_outputs) + sizeof(uint32_t)] = {};
+  uint64_t gepoch = 0, seen_epoch = 0;
   ~eik_plan() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (st_cap) cudaStreamDestroy(st_cap);
     for (void* q : p2p_opened) cudaIpcCloseMemHandle(q);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -791,10 +806,71 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
 
 extern "C" {
 
+static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream);
+
+// Device-resident asynchronous runs (no host buffers, no sync, no profiling)
+// repeated with identical arguments are replayed as one CUDA graph: the
+// second identical call is captured on the plan's private stream (the caller's
+// may be the legacy default stream, which cannot be captured) and every later
+// one is a single cudaGraphLaunch into the caller's stream.  Any plan-buffer
+// allocation in between (g_alloc_epoch) or an argument change re-runs eagerly.
+// EIK_GRAPH=0 turns this off.
 int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream) {
   if (!p || !in || !out) return fail(EIK_EVALIDATION, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   CK(cudaSetDevice(p->device));
+  static const bool graphs = [] {
+    const char* e = std::getenv("EIK_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  const bool graphable = graphs && !(flags & (EIK_HOST_INPUTS | EIK_HOST_OUTPUTS | EIK_SYNC | EIK_CHECK_UNDERFLOW |
+                                              EIK_PROFILE | EIK_SLAB_P2P)) &&
+                         !out->n_underflow && !p->copies_pending;
+  if (!graphable) return run_locked(p, in, out, flags, stream);
+  unsigned char key[sizeof(p->gkey)];
+  std::memcpy(key, in, sizeof(eik_inputs));
+  std::memcpy(key + sizeof(eik_inputs), out, sizeof(eik_outputs));
+  std::memcpy(key + sizeof(eik_inputs) + sizeof(eik_outputs), &flags, sizeof(flags));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t epoch = g_alloc_epoch.load();
+  if (p->gexec && p->gkey_valid && p->gepoch == epoch && !std::memcmp(key, p->gkey, sizeof(key))) {
+    for (bool& u : p->ev_used) u = false;  // no pass times for this run (as for any unprofiled run)
+    CK(cudaGraphLaunch(p->gexec, st));
+    return EIK_OK;
+  }
+  if (!(p->seen_valid && p->seen_epoch == epoch && !std::memcmp(key, p->seen, sizeof(key)))) {
+    std::memcpy(p->seen, key, sizeof(key));
+    p->seen_valid = true;
+    const int rc = run_locked(p, in, out, flags, stream);
+    p->seen_epoch = g_alloc_epoch.load();
+    return rc;
+  }
+  // second identical call: capture it
+  if (!p->st_cap) CK(cudaStreamCreateWithFlags(&p->st_cap, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(p->st_cap, cudaStreamCaptureModeRelaxed));
+  const int rc = run_locked(p, in, out, flags, p->st_cap);
+  const cudaError_t ce = cudaStreamEndCapture(p->st_cap, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CK(ce);
+  if (p->gexec) {
+    cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+  }
+  const cudaError_t ie = cudaGraphInstantiate(&p->gexec, g, 0);
+  cudaGraphDestroy(g);
+  CK(ie);
+  std::memcpy(p->gkey, key, sizeof(key));
+  p->gkey_valid = true;
+  p->gepoch = g_alloc_epoch.load();
+  CK(cudaGraphLaunch(p->gexec, st));
+  return EIK_OK;
+}
+
+static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream) {
   p->run_gen = p->run_gen == INT_MAX ? 1 : p->run_gen + 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t B = in->batch < 1 ? 1 : in->batch;

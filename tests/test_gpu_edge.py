@@ -365,3 +365,70 @@ np.savez(sys.argv[1], **res)
             outs.append(np.load(f))
         for k in outs[0].files:
             assert np.array_equal(outs[0][k], outs[1][k], equal_nan=True), k
+
+
+def test_graph_replay_matches_eager(cuda_ok):
+    """Repeated device-resident runs are captured once and replayed as a CUDA
+    graph (eik_run): replays are bit-identical to eager host runs, read the
+    current contents of the input buffers, and a changed argument (another
+    output buffer) runs eagerly again."""
+    import torch
+
+    from paper_1112_3010_b200 import _native, engine
+
+    grid = _grid((96, 80))
+    N = grid.num_nodes
+    rng = rng_for(123)
+    na = np.sort(rng.choice(N, 60, replace=False)).astype(np.int64)
+    nb = np.sort(rng.choice(N, 60, replace=False)).astype(np.int64)
+    dt = engine.DistanceTransform(grid, 1.5, grad=True, hess=True)
+    ref = {"a": dt.run_host(na), "b": dt.run_host(nb)}
+    plan = _native.Plan(2, grid.counts, 1.0, 1.5, engine.field_bits(2, True, True, False), 0)
+    dev = torch.device("cuda", 0)
+    nodes = torch.from_numpy(na).to(dev)
+    f = lambda: torch.empty(N, dtype=torch.float64, device=dev)  # noqa: E731
+    S, S2, grad, hess = f(), f(), [f(), f()], [f(), f(), f()]
+    # eager, captured, replay, replay on new buffer contents, replay, new S buffer (eager), back
+    for i, (which, out) in enumerate([("a", S), ("a", S), ("a", S), ("b", S), ("a", S), ("a", S2), ("b", S)]):
+        nodes.copy_(torch.from_numpy(na if which == "a" else nb))
+        out.fill_(-1.0)
+        plan.run(nodes, S=out, grad=grad, hess=hess, host=False)
+        torch.cuda.synchronize()
+        r = ref[which]
+        assert np.array_equal(out.cpu().numpy(), r["S"], equal_nan=True), i
+        for a in range(2):
+            assert np.array_equal(grad[a].cpu().numpy(), r["grad"][a], equal_nan=True), i
+        for a in range(3):
+            assert np.array_equal(hess[a].cpu().numpy(), r["hess"][a], equal_nan=True), i
+
+
+def test_graph_replay_with_sign_group(cuda_ok):
+    """The captured graph of a 2-D run with the sign group (forked onto the
+    plan's side stream and joined back) replays bit-identically."""
+    import torch
+
+    from paper_1112_3010_b200 import _native, engine, workloads
+
+    d = workloads.c2(seed=2, n=256, k=2048, radius=80.0, tau=1.0)
+    grid = d["grid"]
+    N = grid.num_nodes
+    dt = engine.DistanceTransform(grid, 1.0, grad=True, hess=True, sign=True)
+    sn, sw = dt.sign_inputs(d["curve"])
+    nd = d["points"].distinct_nodes()
+    ref = dt.run_host(nd, sign_nodes=sn, sign_weights=sw)
+    plan = _native.Plan(2, grid.counts, grid.spacing, 1.0, engine.field_bits(2, True, True, True), 0)
+    dev = torch.device("cuda", 0)
+    nodes, snodes, sweights = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (nd, sn, sw))
+    f = lambda: torch.empty(N, dtype=torch.float64, device=dev)  # noqa: E731
+    S, mu, grad, hess = f(), f(), [f(), f()], [f(), f(), f()]
+    mask = torch.empty(N, dtype=torch.uint8, device=dev)
+    for i in range(4):
+        S.fill_(-1.0)
+        mu.fill_(-1.0)
+        plan.run(nodes, None, 1, snodes, sweights, S=S, grad=grad, hess=hess, mu=mu, mask=mask, host=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(S.cpu().numpy(), ref["S"], equal_nan=True), i
+        assert np.array_equal(mu.cpu().numpy(), ref["mu"]), i
+        assert np.array_equal(mask.cpu().numpy(), ref["mask"]), i
+        for a in range(3):
+            assert np.array_equal(hess[a].cpu().numpy(), ref["hess"][a], equal_nan=True), i
