@@ -20,6 +20,11 @@
  *     buffers itself (pinned host memory gives the best copy rate);
  *   - status codes: 0 ok, 1 validation, 2 underflow (phi <= 0 somewhere;
  *     only reported when EIK_CHECK_UNDERFLOW is set), 3 CUDA/OOM;
+ *   - device-resident asynchronous eik_run calls (no EIK_HOST_*, EIK_SYNC,
+ *     EIK_CHECK_UNDERFLOW, EIK_PROFILE, n_underflow) repeated with identical
+ *     arguments are replayed as one CUDA graph from the second call on (the
+ *     buffers' contents may change between calls, their addresses may not;
+ *     environment EIK_GRAPH=0 disables this);
  *   - a plan is reentrant for calls on one stream at a time; distinct plans are
  *     independent.  No floating-point atomics are used on value paths, so
  *     results are bit-reproducible run to run.
