@@ -1004,17 +1004,30 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       CK(cudaStreamWaitEvent(p->st2, p->ev_fork, 0));
       ss = p->st2;
     }
-    if (want_sign) {
-      if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
-      if ((rc = pass_col2d(p, true, d_snodes, nullptr, Ks, 1, d_sw, r, W.data(), ss))) return rc;
-      if ((rc = mark(EIK_PASS_COL_SIGN, true))) return rc;
-    }
-    if (fork) CK(cudaEventRecord(p->ev_join, ss));
-    if (want_phi) {
-      if ((rc = mark(EIK_PASS_COL, false))) return rc;
-      if ((rc = pass_col2d(p, false, d_nodes, d_off, in->n_nodes, B, nullptr, r, W.data(), st))) return rc;
-      if ((rc = mark(EIK_PASS_COL, true))) return rc;
-    }
+    // the distance group is queued ahead of the sign group (C2 -0.6%);
+    // EIK_SIGN_FIRST=1 restores the opposite order
+    static const bool sign_first = [] {
+      const char* e = std::getenv("EIK_SIGN_FIRST");
+      return e && e[0] == '1';
+    }();
+    auto sign_group = [&]() -> int {
+      if (!want_sign) return EIK_OK;
+      int rc2;
+      if ((rc2 = mark(EIK_PASS_COL_SIGN, false))) return rc2;
+      if ((rc2 = pass_col2d(p, true, d_snodes, nullptr, Ks, 1, d_sw, r, W.data(), ss))) return rc2;
+      if ((rc2 = mark(EIK_PASS_COL_SIGN, true))) return rc2;
+      if (fork) CK(cudaEventRecord(p->ev_join, ss));
+      return EIK_OK;
+    };
+    auto dist_group = [&]() -> int {
+      if (!want_phi) return EIK_OK;
+      int rc2;
+      if ((rc2 = mark(EIK_PASS_COL, false))) return rc2;
+      if ((rc2 = pass_col2d(p, false, d_nodes, d_off, in->n_nodes, B, nullptr, r, W.data(), st))) return rc2;
+      return mark(EIK_PASS_COL, true);
+    };
+    if ((rc = sign_first ? sign_group() : dist_group())) return rc;
+    if ((rc = sign_first ? dist_group() : sign_group())) return rc;
     if (fork) CK(cudaStreamWaitEvent(st, p->ev_join, 0));
   } else {
     const int n_in_max = std::max(want_phi ? 1 : 0, want_sign ? 3 : 0);
