@@ -169,8 +169,13 @@ struct eik_plan {
     if (ev_copies) cudaEventDestroy(ev_copies);
   }
 
+  // Row stride (complex elements) of the 2-D row-major intermediates T and U_j:
+  // H rounded up to 8 (128 bytes), so every row starts on a cache line and the
+  // column kernels' 2- / 4-line warp accesses are whole, aligned sectors (with
+  // H = M/2 + 1 odd rows began 16 bytes into a sector)
+  int64_t rs() const { return D == 2 ? (H + 7) & ~int64_t(7) : H; }
   int64_t comp_elems() const {  // complex elements of one component of one item
-    return D == 2 ? (int64_t)c[0] * H : (int64_t)c[0] * M[1] * H;
+    return D == 2 ? (int64_t)c[0] * rs() : (int64_t)c[0] * M[1] * H;
   }
   int64_t held() const {
     int64_t b = p2p.bytes + tw.bytes + comp.bytes + vin.bytes + trows.bytes + tsign.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
@@ -536,7 +541,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
   const bool rowdft = rowdft_env == 1 || (rowdft_env == 2 && !sg);
   if (rowdft && p->H <= (int64_t)ROWDFT_NF * ROWDFT_NT) {
     DevBuf& T = sg ? p->tsign : p->trows;
-    const int64_t per = (int64_t)p->c[0] * p->H;
+    const int64_t per = (int64_t)p->c[0] * p->rs();
     CK(T.ensure((size_t)n_in * B * per * sizeof(double2)));
     RowDftArgs ra{};
     ra.rowptr = rowptr;
@@ -553,7 +558,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     // per CTA (the sign group): its warp loads are then contiguous runs of a
     // column instead of one 16-byte half sector per row
     const bool tt = (EIK_T_TRANSPOSE >> (sg ? 0 : 1)) & 1;
-    ra.out_rs = tt ? 1 : p->H;
+    ra.out_rs = tt ? 1 : p->rs();
     ra.out_ks = tt ? p->c[0] : 1;
     ra.last_shift = p->lmax - p->L[1];
     ra.last_mask = p->M[1] - 1;
@@ -565,10 +570,10 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     a.n_out = p->c[0];
     a.n_in = n_in;
     for (int i = 0; i < n_in; ++i) a.din[i] = ra.out[i];
-    a.din_es = tt ? 1 : p->H;
+    a.din_es = tt ? 1 : p->rs();
     a.din_ls = tt ? p->c[0] : 1;
     a.din_item = per;
-    a.out_es = p->H;
+    a.out_es = p->rs();
     a.out_item = p->comp_elems();
     set_components(p, sg, r, a, W, 0);
     return sg ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st)
@@ -585,7 +590,7 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
   a.n_valid = p->c[0];
   a.n_out = p->c[0];
   a.rows_per_item = p->c[0];
-  a.out_es = p->H;
+  a.out_es = p->rs();
   a.out_item = p->comp_elems();
   set_components(p, sg, r, a, W, 0);
   return sg ? launch_col<IN_SPARSE, OUT_SUM, true>(p->L[0], a, B, st)
@@ -746,7 +751,7 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
     ra.rows = p->c[0];
     ra.rows_a = p->c[0];
     ra.stride_a = 0;
-    ra.stride_b = H;
+    ra.stride_b = p->rs();
     ra.split_shift = NOSPLIT;
     ra.split_stride = 0;
     ra.comp_item = p->comp_elems();
@@ -1394,7 +1399,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
                       p->rowptr, st);
   if (rc) return rc;
   // impulse DFT once; every chunk of <= 8 taus reuses T
-  CK(p->trows.ensure((size_t)p->c[0] * p->H * sizeof(double2)));
+  CK(p->trows.ensure((size_t)p->c[0] * p->rs() * sizeof(double2)));
   RowDftArgs rd{};
   rd.rowptr = p->rowptr.as<int64_t>();
   rd.cols = p->cols.as<int32_t>();
@@ -1402,7 +1407,9 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
   rd.out[0] = p->trows.as<double2>();
   rd.rows_per_item = p->c[0];
   rd.H = p->H;
-  rd.out_item = (int64_t)p->c[0] * p->H;
+  rd.out_item = (int64_t)p->c[0] * p->rs();
+  rd.out_rs = p->rs();
+  rd.out_ks = 1;
   rd.last_shift = p->lmax - p->L[1];
   rd.last_mask = p->M[1] - 1;
   rd.tw = p->tw.as<double2>();
@@ -1418,9 +1425,9 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
     a.n_out = p->c[0];
     a.n_in = 1;
     a.din[0] = p->trows.as<double2>();
-    a.din_es = p->H;
+    a.din_es = p->rs();
     a.din_item = 0;
-    a.out_es = p->H;
+    a.out_es = p->rs();
     a.out_item = ce;
     a.n_comp = nc;
     for (int j = 0; j < nc; ++j) {
@@ -1431,7 +1438,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
     RowArgs ra{};
     ra.rows = p->c[0];
     ra.rows_a = p->c[0];
-    ra.stride_b = p->H;
+    ra.stride_b = p->rs();
     ra.split_shift = NOSPLIT;
     ra.comp_item = ce;
     ra.n_out = p->c[1];
