@@ -485,7 +485,7 @@ def main():
 
     # kernels per step: per group prep_nodes + rowptr + impulse_rows + column pass;
     # + row pass (3-D: + axis-1 lines before/after the axis-0 pass)
-    launches_per_step = {"C1": 5, "C2": 9, "C3": 7, "C5": 5}[a.config]
+    launches_per_step = {"C1": 4, "C2": 7, "C3": 6, "C5": 4}[a.config]  # prep_nodes, impulse rows, column, (lines), row per group
     if rank == 0:
         line = {
             "metric": "grid points/sec (S+grad S+sign)", "value": value, "unit": "grid_points/s", "n_gpus": world,
@@ -570,7 +570,7 @@ def bench_sweep(a):
                       "unit": "grid_points*taus/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
                       "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                       "dtype": "f64", "data": "synthetic", "config": {"workload": "TS", "taus": taus},
-                      "gpu_launches": 7 * a.steps, "clocks": clk.summary()}))
+                      "gpu_launches": 6 * a.steps, "clocks": clk.summary()}))
     return 0
 
 
@@ -679,7 +679,7 @@ def bench_c4(a):
                        "l2": "working set >> L2", "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": grid.num_nodes * ke / (e2e_ms / 1e3), "unit": "grid_points/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ke},
-            "gpu_launches": 12 * a.steps,
+            "gpu_launches": 10 * a.steps,
             "roofline": None,
             "cpu_baseline": {"value": None, "unit": "grid_points/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": "infeasible: the reference pads to 3072^3 (464 GB per complex array) and "
