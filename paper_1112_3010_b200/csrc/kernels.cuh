@@ -106,6 +106,8 @@ struct ColCfg {
   static constexpr int NT = (col_threads(L) > TPL0) ? col_threads(L) : TPL0;
   static constexpr int LPC = NT / TPL0;
   static constexpr int IL = col_il(LPC);
+  static constexpr bool PFOLD = false;  // register-order spectra unfolded (see TmCfg::PFOLD)
+  static constexpr int NTP = NT;
   using LN = PaddedLine<L, col_e(L), col_pad(L, IL == 2 && LPC > 2)>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
@@ -252,13 +254,29 @@ __device__ __forceinline__ double kload(const KSpec& k, int64_t l, int k0, int M
 }
 // All EPT kernel-spectrum values of this thread for a kernel of configuration
 // CFG (one uniform branch on the layout, outside the unrolled loads).
+// Column of the register-order spectrum copy this thread reads (and whether in
+// reversed register order): itself, or its mirror thread under CFG::PFOLD.
+template <class CFG>
+__device__ __forceinline__ void perm_thread(int& tc, int& rev) {
+  tc = threadIdx.x;
+  rev = 0;
+  if constexpr (CFG::PFOLD) {
+    if (tc >= CFG::NTP) {
+      const int t = tc >> 1, line = tc & 1, a = t >> 4, b = t & 15;
+      tc = 2 * (((16 - a) << 4) | (15 - b)) + line;
+      rev = 1;
+    }
+  }
+}
 template <class CFG>
 __device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpec& k, int64_t l, int t) {
   using LN = typename CFG::LN;
   if (k.perm) {
-    const double* __restrict__ src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NT + threadIdx.x;
+    int tc, rev;
+    perm_thread<CFG>(tc, rev);
+    const double* __restrict__ src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NTP + tc;
 #pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) kn[r] = __ldg(src + r * CFG::NT);
+    for (int r = 0; r < LN::EPT; ++r) kn[r] = __ldg(src + (rev ? LN::EPT - 1 - r : r) * CFG::NTP);
   } else {
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(k, l, LN::out_idx(t, r), LN::M);
@@ -273,9 +291,11 @@ template <class CFG>
 __device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t) {
   using LN = typename CFG::LN;
   if (k.perm) {
-    const double* src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NT + threadIdx.x;
+    int tc, rev;
+    perm_thread<CFG>(tc, rev);
+    const double* src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NTP + tc;
 #pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) prefetch_l1(src + r * CFG::NT);
+    for (int r = 0; r < LN::EPT; ++r) prefetch_l1(src + r * CFG::NTP);
   } else {
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) {
@@ -506,6 +526,9 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_SPF
 #define EIK_SPF 1
 #endif
+#ifndef EIK_PFOLD
+#define EIK_PFOLD 0
+#endif
 #ifndef EIK_TWC
 #define EIK_TWC 1
 #endif
@@ -533,6 +556,15 @@ struct TmCfg {
   using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
+  // Folded register-order kernel spectra (four-step lines, two lanes-interleaved
+  // lines): thread t = 16 a + b holds k0 = a + 16 b + 256 r, whose mirror
+  // M - k0 is held by thread 16 (16 - a) + 15 - b at register 15 - r.  Warps
+  // 0-8 (a <= 8) own the stored copy (NTP = 288 of 512 threads per register
+  // row); warps 9-15 read their mirror's entries, in reversed lane order
+  // (still whole contiguous segments), and the odd-kernel sign of k0 > M/2 is
+  // applied at use.  9/16 of the unfolded bytes.
+  static constexpr bool PFOLD = EIK_PFOLD && F4K && NT == 512 && IL == 2 && LPC == 2;
+  static constexpr int NTP = PFOLD ? 288 : NT;
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
   // 4096-point lines: the radix-16 NS=256 stage's twiddles W^{t r} are per-thread
   // constants shared by the forward and every inverse -> cached in TMEM too
@@ -555,7 +587,7 @@ struct TmCfg {
   // bulk-copied into shared memory one transform ahead, where it fits next to
   // MINB resident CTAs (C2: 64 KB on top of 158 KB, one CTA per SM).
   static constexpr size_t KFEED_BYTES = (size_t)LN::EPT * NT * sizeof(double);
-  static constexpr bool KFEED = EIK_KFEED && (SMEM_BYTES + 16 + KFEED_BYTES) * MINB <= 227 * 1024;
+  static constexpr bool KFEED = EIK_KFEED && !PFOLD && (SMEM_BYTES + 16 + KFEED_BYTES) * MINB <= 227 * 1024;
   static constexpr size_t SMEM_FEED_BYTES = SMEM_BYTES + (KFEED ? 16 + KFEED_BYTES : 0);
   // SUM kernels (sign group): the next input line (half-padded: EPT/2 values
   // per thread, thread-private slots) is staged with cp.async while the
@@ -909,8 +941,8 @@ __global__ void spectrum_perm_kernel(const double* __restrict__ re, int64_t ld, 
                                      double* __restrict__ kp, int64_t total) {
   using LN = typename CFG::LN;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int tid = (int)(i % CFG::NT);
-    const int64_t rest = i / CFG::NT;
+    const int tid = (int)(i % CFG::NTP);
+    const int64_t rest = i / CFG::NTP;
     const int r = (int)(rest % LN::EPT);
     const int64_t b = rest / LN::EPT;
     const int64_t l = b * CFG::LPC + CFG::line_of(tid);
@@ -919,7 +951,7 @@ __global__ void spectrum_perm_kernel(const double* __restrict__ re, int64_t ld, 
     double v = 0.0;
     if (l < nlines) {
       v = re[(int64_t)(hi ? LN::M - k0 : k0) * ld + l];
-      if (odd0 && hi) v = -v;
+      if (odd0 && hi && !CFG::PFOLD) v = -v;  // folded copies: sign applied at use
     }
     kp[i] = v;
   }

@@ -39,7 +39,7 @@ int launch_col(int L, const ColArgs& a, int64_t items, cudaStream_t st);
 template <bool INV, bool HALF>
 int launch_lines(int L, const LinesArgs& a, int ncomp, cudaStream_t st);
 int launch_spectrum_perm(int L, bool sum, const double* re, int64_t ld, int64_t nlines, int odd0, double* kp, int64_t* elems,
-                         cudaStream_t st);
+                         int* folded, cudaStream_t st);
 int launch_row(int LH, const RowArgs& a, int64_t items, cudaStream_t st);
 int launch_r2c(int LH, const GenArgs& g, int64_t nrows, double2* out, int64_t out_rs, const double2* tw, int lmax,
                cudaStream_t st);

@@ -94,10 +94,12 @@ int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
 // Register-order spectrum for the column kernel launch_col picks at length 2^L
 // for real spectra (COMPS / SUM).  kp == nullptr: only report the size.
 template <class C>
-int permute_t(const double* re, int64_t ld, int64_t nlines, int odd0, double* kp, int64_t* elems, cudaStream_t st) {
+int permute_t(const double* re, int64_t ld, int64_t nlines, int odd0, double* kp, int64_t* elems, int* folded,
+              cudaStream_t st) {
   const int64_t tiles = (nlines + C::LPC - 1) / C::LPC;
-  const int64_t total = tiles * C::LN::EPT * C::NT;
+  const int64_t total = tiles * C::LN::EPT * C::NTP;
   *elems = total;
+  *folded = C::PFOLD ? 1 : 0;
   if (!kp || total == 0) return EIK_OK;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 64);
   spectrum_perm_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(re, ld, nlines, odd0, kp, total);
@@ -106,14 +108,14 @@ int permute_t(const double* re, int64_t ld, int64_t nlines, int odd0, double* kp
 }
 
 int launch_spectrum_perm(int L, bool sum, const double* re, int64_t ld, int64_t nlines, int odd0, double* kp,
-                         int64_t* elems, cudaStream_t st) {
+                         int64_t* elems, int* folded, cudaStream_t st) {
 #define EIK_PERM(Lc)                                                                                     \
   if constexpr (Lc >= 9) {                                                                               \
     if (use_tmem())                                                                                      \
-      return sum ? permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_SUM)>>(re, ld, nlines, odd0, kp, elems, st)       \
-                 : permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_COMPS)>>(re, ld, nlines, odd0, kp, elems, st);    \
+      return sum ? permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_SUM)>>(re, ld, nlines, odd0, kp, elems, folded, st)       \
+                 : permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_COMPS)>>(re, ld, nlines, odd0, kp, elems, folded, st);    \
   }                                                                                                      \
-  return permute_t<ColCfg<Lc>>(re, ld, nlines, odd0, kp, elems, st)
+  return permute_t<ColCfg<Lc>>(re, ld, nlines, odd0, kp, elems, folded, st)
   EIK_SWITCH_L(L, EIK_PERM);
 #undef EIK_PERM
   return EIK_OK;

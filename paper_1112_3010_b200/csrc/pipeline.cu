@@ -108,6 +108,7 @@ struct KDev {
   double sign = 1.0;
   DevBuf buf;  // folded real/imag spectrum [(M0/2+1) x lines]
   DevBuf kp;   // register-order copy for the 2-D column kernels (KSpec::perm), or empty
+  bool kp_folded = false;  // kp holds mirrored k0 once (TmCfg::PFOLD): odd-kernel sign applied at use
 };
 
 }  // namespace
@@ -322,12 +323,15 @@ int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, in
   if (rc) return rc;
   if (p->D == 2 && p->ks_l0 == 0 && p->ks_lines == p->lines) {
     int64_t elems = 0;
+    int folded = 0;
     const bool sum = &v == &p->ksign;  // the sign group runs the SUM column kernel
-    if ((rc = launch_spectrum_perm(p->L[0], sum, nullptr, 0, p->ks_lines, 0, nullptr, &elems, st))) return rc;
+    if ((rc = launch_spectrum_perm(p->L[0], sum, nullptr, 0, p->ks_lines, 0, nullptr, &elems, &folded, st)))
+      return rc;
     CK(k->kp.ensure(elems * sizeof(double)));
     if ((rc = launch_spectrum_perm(p->L[0], sum, k->buf.as<double>(), p->ks_lines, p->ks_lines, k->odd0,
-                                   k->kp.as<double>(), &elems, st)))
+                                   k->kp.as<double>(), &elems, &folded, st)))
       return rc;
+    k->kp_folded = folded != 0;
   }
   v.push_back(std::move(k));
   return EIK_OK;
@@ -341,7 +345,7 @@ KSpec kspec_of(const eik_plan* p, const KDev& k) {
   s.odd0 = k.odd0;
   if (k.kp.bytes) {
     s.perm = k.kp.as<double>();
-    s.odd0 = 0;
+    s.odd0 = k.kp_folded ? k.odd0 : 0;
   }
   return s;
 }
