@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v $(EXTRA)
 SRC := paper_1112_3010_b200/csrc
 OBJ := build/obj
 LIB := paper_1112_3010_b200/_lib/libeikfld_b200.so
-UNITS := pipeline launch_col_sparse launch_col_dense launch_col_spec launch_lines launch_rows classify dd_pipeline
+UNITS := pipeline launch_col_sparse launch_col_dense launch_col_spec launch_lines launch_rows classify dd_pipeline spectral
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(UNITS))) $(OBJ)/dd_twiddle.o
 HDRS := $(wildcard $(SRC)/*.cuh) include/eikfld_b200.h
 

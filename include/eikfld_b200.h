@@ -95,7 +95,9 @@ typedef struct {
   double* grad[3];    /* S_a = (f_a exp * delta)/(exp * delta), reference axis order */
   double* hess[3];    /* S_xx, S_yy, S_xy (2-D) */
   double* mu;         /* winding (2-D) or degree (3-D) field */
-  uint8_t* mask;      /* rint(mu) > 0 (2-D) / rint(mu) >= 1 (3-D), unflagged rule of R/sign.py:190-195 */
+  uint8_t* mask;      /* classify(mu) of R/sign.py:166-198: rint(mu) > 0 (2-D) / rint(mu) >= 1 (3-D), the
+                         flagged (sign) nodes taking their nearest unflagged node's class with
+                         scipy's EDT ties (eik_run; slab ranks: eik_slab_fill) */
   uint8_t* underflow; /* 1 where phi <= 0 */
   int64_t* n_underflow;        /* host scalar, written when the call synchronizes */
   unsigned long long* d_underflow_count; /* optional device counter (accumulated) */
@@ -174,6 +176,19 @@ int eik_slab_p2p_init(eik_plan* plan, int world, int rank, int64_t c0_local, int
                       int64_t* arena_bytes, void* ipc_handle);
 int eik_slab_p2p_connect(eik_plan* plan, void* const* peer_arenas, const void* ipc_handles);
 
+/* Flagged-node fill of a slab rank's sign mask (the classify step of
+ * R/sign.py:179-195, which eik_run performs internally): eik_slab_finish
+ * classifies every owned node by its own mu; this call then gives each owned
+ * flagged node the class of its nearest unflagged node, with scipy EDT ties.
+ * The nearest node may lie on a neighbour's planes, so the caller passes a
+ * halo-extended copy of the mask, planes [e0, e1) (own planes
+ * [own0, own0 + c0_local) plus neighbour planes), and every flagged node of
+ * those planes (ext_nodes: sorted flat indices relative to plane e0).  Device
+ * buffers; synchronous.  Returns EIK_EVALIDATION if a search needs a plane
+ * outside [e0, e1) (widen the halo and call again). */
+int eik_slab_fill(eik_plan* plan, const int64_t* ext_nodes, int64_t n_ext, int64_t e0, int64_t e1, int64_t own0,
+                  int64_t c0_local, const uint8_t* mask_ext, uint8_t* mask_own, void* stream);
+
 /* Extended-precision (double-double, ~106-bit) convolution (SURVEY.md §8(f)
  * rank 4): the big-float path of R/convolution.py:67-143 with p = 106, used by
  * the drop-in API for PrecisionConfig.bigfloat(tau, bits <= 106).  Fields:
@@ -218,6 +233,31 @@ int eik_run_sweep(eik_plan* plan, const int64_t* nodes, int64_t n_nodes, double*
 int eik_classify(int dim, const int64_t* counts, const double* mu, const int64_t* flagged_nodes, int64_t n_flagged,
                  int mode, int use_threshold, double threshold, double* out_mask, const double* S,
                  double* out_signed, uint32_t flags, int device, void* stream);
+
+/* Engine-level spectral API (R/convolution.py:164-313), for callers of the
+ * reference's FftConvolver building blocks.  Arrays of any shape (each axis
+ * >= 1; mixed-radix Stockham transforms, Bluestein for prime factors > 31);
+ * complex arrays are interleaved (re, im) float64, row-major.  Host or device
+ * buffers (EIK_HOST_INPUTS / EIK_HOST_OUTPUTS); synchronous when host buffers
+ * are used.  The reference's 2^31-element cap (_check_sizes) is lifted.
+ *   eik_fftn         unnormalised forward DFT over every axis (fft_forward,
+ *                    164-169), or the 1/P-normalised inverse (fft_inverse,
+ *                    172-177); in_real: `in` is real float64.
+ *   eik_fft_pair     forward_pair (264-286): the spectra of two real arrays
+ *                    zero-padded to pshape, from one complex transform
+ *                    (a or b may be NULL = zeros).
+ *   eik_ifft_window  inverse_to_grid / inverse_pair_to_grid (288-307): inverse
+ *                    of hat_a (+ i hat_b), window [start, start + counts) per
+ *                    axis, real (and imaginary) parts.
+ *   eik_cmul         product (309-313): elementwise complex multiply. */
+int eik_fftn(int ndim, const int64_t* shape, const double* in, int in_real, double* out, int inverse, uint32_t flags,
+             int device, void* stream);
+int eik_fft_pair(int ndim, const int64_t* pshape, const double* a, const int64_t* ashape, const double* b,
+                 const int64_t* bshape, double* a_hat, double* b_hat, uint32_t flags, int device, void* stream);
+int eik_ifft_window(int ndim, const int64_t* pshape, const double* hat_a, const double* hat_b,
+                    const int64_t* window_start, const int64_t* window_counts, double* out_re, double* out_im,
+                    uint32_t flags, int device, void* stream);
+int eik_cmul(int64_t n, const double* a, const double* b, double* out, uint32_t flags, int device, void* stream);
 
 /* Device milliseconds of each pass of the last eik_run issued with
  * EIK_PROFILE (synchronizes on its events); -1 for passes that did not run. */

@@ -34,7 +34,7 @@ __all__ = [
     "hessian_2d_unchecked", "snap", "tangent_impulses", "flux_impulses",
     "winding_field", "degree_field", "classify", "s_direct", "direct_ratios",
     "winding_direct", "degree_direct", "hessian_factors", "OracleUnderflow",
-    "run_config_unchecked", "phi_direct_mp",
+    "run_config_unchecked", "phi_direct_mp", "degree_from_weights", "direct_local",
 ]
 
 
@@ -312,6 +312,61 @@ def degree_field(triangles, centers, normals, origin, spacing, counts):
     h = k0 * g0 + k1 * g1 + k2 * g2
     mu = conv.inverse_to_grid(h)
     return -mu.reshape(-1) / (4.0 * math.pi), flagged
+
+
+def degree_from_weights(nodes, weights, spacing, counts):
+    """degree_field's convolution (R/sign.py:135-163) fed per-node weight vectors
+    (nodes: distinct flat indices; weights: (3, len(nodes)), already summed per
+    node as FluxData.build's np.add.at does) instead of triangle centres: the
+    C4 workload's vertex normals.  Same kernels, packing and order."""
+    n = int(np.prod(counts))
+    gs = []
+    for a in range(3):
+        g = np.zeros(n)
+        g[np.asarray(nodes, dtype=np.int64)] = weights[a]
+        gs.append(g)
+    ks = [ratio_kernel(counts, spacing, a, 3) for a in range(3)]
+    conv = Convolver(counts, ks[0].shape)
+    k0, k1 = conv.forward_pair(ks[0], ks[0].shape, ks[1], ks[1].shape)
+    k2, g0 = conv.forward_pair(ks[2], ks[2].shape, gs[0].reshape(counts), counts)
+    g1, g2 = conv.forward_pair(gs[1].reshape(counts), counts, gs[2].reshape(counts), counts)
+    h = k0 * g0 + k1 * g1 + k2 * g2
+    mu = conv.inverse_to_grid(h)
+    return -mu.reshape(-1) / (4.0 * math.pi)
+
+
+def direct_local(src, query, tau, hessian=False, cutoff=30.0):
+    """s_direct / direct_ratios (R/distance.py:133-152, R/derivatives.py:186-207)
+    at selected query points, summing only the sources within dmin + cutoff of
+    each query (kd-tree).  The dropped terms carry weight exp(-cutoff/tau) or
+    less relative to the nearest one (cutoff 30, tau 0.5: e^-60), far below
+    float64 resolution, so this equals the full sums; it makes the exact
+    checker affordable at C3 scale.  Returns (S, [ratios...])."""
+    from scipy.spatial import cKDTree
+
+    src = np.asarray(src, dtype=np.float64)
+    query = np.atleast_2d(np.asarray(query, dtype=np.float64))
+    tree = cKDTree(src)
+    dmin, _ = tree.query(query)
+    S = np.empty(query.shape[0])
+    nf = (5 if hessian else src.shape[1])
+    acc = [np.empty(query.shape[0]) for _ in range(nf)]
+    for q in range(query.shape[0]):
+        idx = tree.query_ball_point(query[q], dmin[q] + cutoff)
+        diff = query[q][None, :] - src[idx]
+        dist = np.sqrt(np.einsum("ij,ij->i", diff, diff))
+        r = dist.min()
+        w = np.exp(-(dist - r) / tau)
+        den = w.sum()
+        S[q] = r - tau * np.log(den)
+        zero = dist == 0.0
+        safe = np.where(zero, 1.0, dist)
+        fa = [np.where(zero, 0.0, diff[:, a] / safe) for a in range(diff.shape[1])]
+        ir = np.where(zero, 0.0, 1.0 / safe)
+        facs = hessian_factors(fa, ir, tau) if hessian else fa
+        for a, f in enumerate(facs):
+            acc[a][q] = (f * w).sum() / den
+    return S, acc
 
 
 def classify(mu, flagged, counts, mode, threshold=None):

@@ -87,12 +87,22 @@ def lib():
                                          C.c_uint32, C.c_void_p]
             L.eik_slab_finish.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs),
                                           C.c_uint32, C.c_void_p]
+            L.eik_slab_fill.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                        C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.eik_fftn.argtypes = [C.c_int, _i64p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_uint32, C.c_int,
+                                   C.c_void_p]
+            L.eik_fft_pair.argtypes = [C.c_int, _i64p, C.c_void_p, _i64p, C.c_void_p, _i64p, C.c_void_p, C.c_void_p,
+                                       C.c_uint32, C.c_int, C.c_void_p]
+            L.eik_ifft_window.argtypes = [C.c_int, _i64p, C.c_void_p, C.c_void_p, _i64p, _i64p, C.c_void_p,
+                                          C.c_void_p, C.c_uint32, C.c_int, C.c_void_p]
+            L.eik_cmul.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p]
             L.eik_last_error.restype = C.c_char_p
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
                          "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
                          "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep",
                          "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect", "eik_dd_plan_create",
-                         "eik_dd_plan_destroy", "eik_dd_run"):
+                         "eik_dd_plan_destroy", "eik_dd_run", "eik_slab_fill", "eik_fftn", "eik_fft_pair",
+                         "eik_ifft_window", "eik_cmul"):
                 getattr(L, name).restype = C.c_int
             _lib = L
         return _lib
@@ -102,7 +112,8 @@ def exported_symbols():
     return ["eik_plan_create", "eik_plan_create_slab", "eik_plan_destroy", "eik_plan_info", "eik_run",
             "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
             "eik_plan_create_sweep", "eik_run_sweep", "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect",
-            "eik_dd_plan_create", "eik_dd_plan_destroy", "eik_dd_run",
+            "eik_dd_plan_create", "eik_dd_plan_destroy", "eik_dd_run", "eik_slab_fill",
+            "eik_fftn", "eik_fft_pair", "eik_ifft_window", "eik_cmul",
             "eik_last_error", "eik_version"]
 
 
@@ -198,6 +209,10 @@ class Plan:
         check(lib().eik_slab_finish(self._h, wa, int(c0_local), int(ks), C.byref(out), SLAB_P2P if p2p else 0,
                                     stream))
 
+    def slab_fill(self, ext_nodes, e0, e1, own0, c0_local, mask_ext, mask_own, stream=None):
+        check(lib().eik_slab_fill(self._h, _ptr(ext_nodes), int(ext_nodes.shape[0]), int(e0), int(e1), int(own0),
+                                  int(c0_local), _ptr(mask_ext), _ptr(mask_own), stream))
+
     def pass_times(self):
         """Device ms per pass of the last profiled run ({name: ms}, absent passes omitted)."""
         ms = (C.c_double * len(PASS_NAMES))()
@@ -205,15 +220,24 @@ class Plan:
         return {n: v for n, v in zip(PASS_NAMES, ms) if v >= 0}
 
     def close(self):
+        """Destroy the native plan; waits for a run in progress on another thread."""
         h = getattr(self, "_h", None)
         if C is None or h is None:  # interpreter shutdown: module globals already gone
             return
-        if h.value:
-            self._h = C.c_void_p()
-            try:
-                lib().eik_plan_destroy(h)
-            except Exception:  # interpreter shutdown: the process releases the device anyway
-                pass
+        lock = getattr(self, "_lock", None)
+        if lock is not None:
+            lock.acquire()
+        try:
+            h = self._h
+            if h.value:
+                self._h = C.c_void_p()
+                try:
+                    lib().eik_plan_destroy(h)
+                except Exception:  # interpreter shutdown: the process releases the device anyway
+                    pass
+        finally:
+            if lock is not None:
+                lock.release()
 
     __del__ = close
 
@@ -280,8 +304,9 @@ def get_plan(grid, tau, fields, device=0) -> Plan:
     with _PLANS_LOCK:
         _PLANS[key] = p
         while len(_PLANS) > _MAX_PLANS:
-            _, old = _PLANS.popitem(last=False)
-            old.close()
+            # dropped, not closed: a thread may still be running on it; the
+            # plan is destroyed by __del__ once the last reference is gone
+            _PLANS.popitem(last=False)
     return p
 
 
@@ -348,12 +373,20 @@ class DDPlan:
         h = getattr(self, "_h", None)
         if C is None or h is None:  # interpreter shutdown: module globals already gone
             return
-        if h.value:
-            self._h = C.c_void_p()
-            try:
-                lib().eik_dd_plan_destroy(h)
-            except Exception:
-                pass
+        lock = getattr(self, "_lock", None)
+        if lock is not None:
+            lock.acquire()
+        try:
+            h = self._h
+            if h.value:
+                self._h = C.c_void_p()
+                try:
+                    lib().eik_dd_plan_destroy(h)
+                except Exception:
+                    pass
+        finally:
+            if lock is not None:
+                lock.release()
 
     __del__ = close
 
@@ -372,8 +405,7 @@ def get_dd_plan(grid, tau, fields, device=0) -> DDPlan:
     with _PLANS_LOCK:
         _DD_PLANS[key] = p
         while len(_DD_PLANS) > 2:  # DD plans are large (32 B per padded point per kernel)
-            _, old = _DD_PLANS.popitem(last=False)
-            old.close()
+            _DD_PLANS.popitem(last=False)  # freed by __del__ once no thread holds it
     return p
 
 
@@ -422,3 +454,58 @@ def classify(counts, mu, flagged, mode, threshold=None, S=None, device=0):
                              None if S is None else S.ctypes.data, None if sd is None else sd.ctypes.data,
                              HOST_INPUTS | HOST_OUTPUTS, device, None))
     return mask, sd
+
+
+# -- engine-level spectral API (R/convolution.py:164-313) -----------------------
+
+def _dims(shape):
+    return (C.c_int64 * max(1, len(shape)))(*[int(x) for x in shape])
+
+
+def fftn(array, inverse=False, device=0):
+    """Forward (unnormalised) or inverse (1/P) DFT over every axis; host arrays, complex128 out."""
+    arr = np.asarray(array)
+    real = not np.iscomplexobj(arr)
+    src = np.ascontiguousarray(arr, dtype=np.float64 if real else np.complex128)
+    out = np.empty(src.shape, dtype=np.complex128)
+    check(lib().eik_fftn(src.ndim, _dims(src.shape), src.ctypes.data, int(real), out.ctypes.data, int(bool(inverse)),
+                         HOST_INPUTS | HOST_OUTPUTS, device, None))
+    return out
+
+
+def fft_pair(pshape, a, ashape, b, bshape, device=0):
+    """forward_pair: spectra of two real arrays zero-padded to pshape (one complex transform)."""
+    a = None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+    b = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+    ah = np.empty(tuple(pshape), dtype=np.complex128)
+    bh = np.empty(tuple(pshape), dtype=np.complex128)
+    check(lib().eik_fft_pair(len(pshape), _dims(pshape), None if a is None else a.ctypes.data, _dims(ashape),
+                             None if b is None else b.ctypes.data, _dims(bshape), ah.ctypes.data, bh.ctypes.data,
+                             HOST_INPUTS | HOST_OUTPUTS, device, None))
+    return ah, bh
+
+
+def ifft_window(hat_a, hat_b, start, counts, want_imag, device=0):
+    """Inverse of hat_a (+ i hat_b) restricted to the window [start, start + counts): (real, imag|None)."""
+    ha = np.ascontiguousarray(hat_a, dtype=np.complex128)
+    hb = None if hat_b is None else np.ascontiguousarray(hat_b, dtype=np.complex128)
+    if hb is not None and hb.shape != ha.shape:
+        raise ValidationError("spectra of different shapes")
+    re = np.empty(tuple(counts))
+    im = np.empty(tuple(counts)) if want_imag else None
+    check(lib().eik_ifft_window(ha.ndim, _dims(ha.shape), ha.ctypes.data, None if hb is None else hb.ctypes.data,
+                                _dims(start), _dims(counts), re.ctypes.data, None if im is None else im.ctypes.data,
+                                HOST_INPUTS | HOST_OUTPUTS, device, None))
+    return re, im
+
+
+def cmul(a, b, device=0):
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    if a.shape != b.shape:
+        a, b = np.broadcast_arrays(a, b)
+        a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    out = np.empty(a.shape, dtype=np.complex128)
+    check(lib().eik_cmul(a.size, a.ctypes.data, b.ctypes.data, out.ctypes.data, HOST_INPUTS | HOST_OUTPUTS, device,
+                         None))
+    return out

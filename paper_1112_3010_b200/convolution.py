@@ -1,15 +1,29 @@
-"""Engine-level zero-padded LINEAR convolution on the GPU.
+"""Engine-level zero-padded LINEAR convolution and transforms on the GPU.
 
 Drop-in for the float64 engine of R/convolution.py: KernelField 30-64,
-FftConvolver 212-366 (convolve, convolve_many), fft_convolve 369-375,
-assert_positive 378-388.  Arbitrary (user) kernels are transformed on the
-device into full complex half-spectra; the field goes through the same
-pruned r2c -> fused column -> c2r passes as the distance pipeline.
+fft_forward / fft_inverse / _check_sizes 164-184, _padded_shape 205-209,
+FftConvolver 212-366 (kernel_hat, impulse_hat, forward_pair,
+inverse_to_grid, inverse_pair_to_grid, product, convolve, convolve_many),
+fft_convolve 369-375, assert_positive 378-388.
 
-Padding differs from the reference by design: each axis is padded to the
-power of two >= 2c-1 (enough for a linear convolution restricted to the grid
-window; SURVEY.md exec. summary item 8) instead of next_fast_len(3c-2), and
-there is no 2^31-element cap.
+Two device paths sit behind this module:
+
+* `convolve` / `convolve_many` run the fused pipeline (csrc/pipeline.cu
+  eik_convolve): pruned r2c -> fused column -> c2r passes over each axis
+  padded to the power of two >= 2c-1, which is enough for a linear
+  convolution restricted to the grid window (SURVEY.md exec. summary item 8),
+  instead of next_fast_len(3c-2);
+* the spectral building blocks (`fft_forward`, `kernel_hat`, `forward_pair`,
+  `inverse_to_grid`, ...) hand spectra back as arrays, so they keep the
+  reference's padded shape `pshape` = next_fast_len(c + k - 1) per axis and
+  its layout (operands at the origin, output window at the kernel centre);
+  their transforms are the mixed-radix / Bluestein device FFTs of
+  csrc/spectral.cu.  Values agree with the reference's to float64 FFT noise.
+
+Divergences: no 2^31-element cap (_check_sizes); big-float configs raise
+ValidationError here (the big-float engine is the reference's CPU path; the
+drop-in's S / gradient entry points run big-float configs up to 106 bits on
+the double-double device path instead).
 """
 
 from __future__ import annotations
@@ -53,6 +67,47 @@ class KernelField:
         return all(s >= 2 * c - 1 for s, c in zip(self.shape, grid.counts))
 
 
+def next_fast_len(target: int) -> int:
+    """Smallest 2^a 3^b 5^c 7^d 11^e >= target: scipy.fft.next_fast_len(target)
+    for complex transforms, which R/convolution.py:209 calls."""
+    n = max(1, int(target))
+    while True:
+        m = n
+        for p in (2, 3, 5, 7, 11):
+            while m % p == 0:
+                m //= p
+        if m == 1:
+            return n
+        n += 1
+
+
+def _check_sizes(shape):
+    """R/convolution.py:180-184 minus the 2^31-element cap (lifted on the device)."""
+    if any(int(s) < 1 for s in shape):
+        raise ValidationError(f"zero-length FFT axis in shape {tuple(shape)}")
+
+
+def fft_forward(array, cfg) -> np.ndarray:
+    """Unnormalized forward DFT over every axis of the array (R/convolution.py:164-169)."""
+    require_native(cfg)
+    arr = np.asarray(array)
+    _check_sizes(arr.shape)
+    return _native.fftn(arr, inverse=False)
+
+
+def fft_inverse(array, cfg) -> np.ndarray:
+    """Inverse DFT normalized by 1/N over every axis (R/convolution.py:172-177)."""
+    require_native(cfg)
+    arr = np.asarray(array)
+    _check_sizes(arr.shape)
+    return _native.fftn(arr, inverse=True)
+
+
+def _padded_shape(grid, kshape, cfg) -> tuple:
+    """next_fast_len(c + k - 1) per axis (R/convolution.py:205-209, float64 mode)."""
+    return tuple(next_fast_len(c + k - 1) for c, k in zip(grid.counts, kshape))
+
+
 class FftConvolver:
     """Reusable linear-convolution plan over one grid (R/convolution.py:212-366)."""
 
@@ -67,7 +122,50 @@ class FftConvolver:
             raise ValidationError("kernel extent must cover the grid extent")
         if any(c < 1 for c in grid.counts):
             raise ValidationError(f"zero-length FFT axis in shape {grid.counts}")
-        self.pshape = tuple(1 << max(1, int(2 * c - 1 - 1).bit_length()) for c in grid.counts)
+        # spectral building blocks: the reference's padded shape and window
+        self.pshape = _padded_shape(grid, self.kshape, cfg)
+        center = tuple(s // 2 for s in self.kshape)
+        self.out_slice = tuple(slice(c, c + n) for c, n in zip(center, grid.counts))
+
+    # -- single transforms (R/convolution.py:244-251)
+
+    def kernel_hat(self, kernel: KernelField) -> np.ndarray:
+        self._check_kernel(kernel)
+        return _native.fft_pair(self.pshape, kernel.values, kernel.shape, None, self.kshape)[0]
+
+    def impulse_hat(self, impulses: ScalarField) -> np.ndarray:
+        g = self._field(impulses).reshape(self.grid.counts)
+        return _native.fft_pair(self.pshape, g, self.grid.counts, None, self.grid.counts)[0]
+
+    # -- packed real transforms (R/convolution.py:264-307)
+
+    def forward_pair(self, a, ashape, b, bshape):
+        """FFTs of two real arrays from one complex transform."""
+        a = np.asarray(a, dtype=np.float64).reshape(tuple(ashape))
+        b = np.asarray(b, dtype=np.float64).reshape(tuple(bshape))
+        return _native.fft_pair(self.pshape, a, a.shape, b, b.shape)
+
+    def inverse_to_grid(self, hat) -> np.ndarray:
+        """Inverse transform restricted to the grid window, real part."""
+        hat = self._spectrum(hat)
+        start = [s.start for s in self.out_slice]
+        return _native.ifft_window(hat, None, start, self.grid.counts, False)[0]
+
+    def inverse_pair_to_grid(self, hat_a, hat_b):
+        """Two inverse transforms of real-sequence spectra in one pass."""
+        start = [s.start for s in self.out_slice]
+        return _native.ifft_window(self._spectrum(hat_a), self._spectrum(hat_b), start, self.grid.counts, True)
+
+    def product(self, a_hat, b_hat) -> np.ndarray:
+        return _native.cmul(a_hat, b_hat)
+
+    def _spectrum(self, hat):
+        hat = np.asarray(hat)
+        if hat.dtype == object:
+            raise ValidationError("the B200 build takes complex128 spectra only")
+        if hat.shape != self.pshape:
+            raise ValidationError(f"spectrum shape {hat.shape} != padded shape {self.pshape}")
+        return hat
 
     def _check_kernel(self, kernel: KernelField):
         if not np.isclose(kernel.spacing, self.grid.spacing, rtol=1e-12, atol=0):

@@ -33,6 +33,13 @@ int eik_fail(int code, const std::string& msg) {
   return code;
 }
 
+// classify.cu: flagged-node fill of the sign mask (R/sign.py:179-189)
+int eik_fill_bits(const int64_t* d_nodes, int64_t K, int64_t N, uint32_t* bits, cudaStream_t st);
+int eik_fill_mask(int dim, const int64_t* counts, const int64_t* d_nodes, int64_t K, const uint32_t* bits,
+                  uint8_t* mask, cudaStream_t st);
+int eik_slab_fill_mask(const int64_t* counts, const int64_t* ext_nodes, int64_t K, int64_t e0, int64_t e1,
+                       int64_t own0, int64_t c0_local, const uint8_t* mask_ext, uint8_t* mask_own, cudaStream_t st);
+
 namespace {
 // bumped on every device allocation of a DevBuf: a captured CUDA graph is
 // replayed only while no plan buffer it references can have moved
@@ -141,6 +148,7 @@ struct eik_plan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr, ev_copies = nullptr;
   bool copies_pending = false;  // EIK_ASYNC: D2H of the last run still reads `stage`
   DevBuf serr, trows, tsign;
+  DevBuf fillbits;  // flagged-node bitmap of the sign nodes (mask fill)
   // peer-to-peer slab exchange: own arena [P2P_NV V slots][n_comp W slots]
   // and every rank's arena base (own, same-process or IPC-opened)
   DevBuf p2p;
@@ -179,7 +187,7 @@ struct eik_plan {
     return D == 2 ? (int64_t)c[0] * rs() : (int64_t)c[0] * M[1] * H;
   }
   int64_t held() const {
-    int64_t b = p2p.bytes + tw.bytes + comp.bytes + vin.bytes + trows.bytes + tsign.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
+    int64_t b = fillbits.bytes + p2p.bytes + tw.bytes + comp.bytes + vin.bytes + trows.bytes + tsign.bytes + rowid.bytes + cols.bytes + rowptr.bytes + srowid.bytes +
                 scols.bytes + srowptr.bytes + stage.bytes + work.bytes + h_nodes.bytes + h_off.bytes +
                 h_snodes.bytes + h_sw.bytes;
     for (auto& k : kdist) b += k->buf.bytes;
@@ -348,6 +356,25 @@ KSpec kspec_of(const eik_plan* p, const KDev& k) {
     s.odd0 = k.kp_folded ? k.odd0 : 0;
   }
   return s;
+}
+
+// Host-side validation of host node lists before anything is queued (so the
+// asynchronous host path reports bad inputs too): item offsets start at 0,
+// never decrease and end at K; nodes are strictly increasing inside [0, N)
+// within each item.
+int host_check_nodes(const int64_t* nodes, int64_t K, const int64_t* off, int64_t B, int64_t N_item) {
+  if (off) {
+    if (off[0] != 0 || off[B] != K) return fail(EIK_EVALIDATION, "item offsets must start at 0 and end at n_nodes");
+    for (int64_t b = 0; b < B; ++b)
+      if (off[b + 1] < off[b]) return fail(EIK_EVALIDATION, "item offsets must be non-decreasing");
+  }
+  for (int64_t b = 0; b < (off ? B : 1); ++b) {
+    const int64_t p0 = off ? off[b] : 0, p1 = off ? off[b + 1] : K;
+    for (int64_t q = p0; q < p1; ++q)
+      if (nodes[q] < 0 || nodes[q] >= N_item || (q > p0 && nodes[q] <= nodes[q - 1]))
+        return fail(EIK_EVALIDATION, "node indices must be sorted, distinct and inside the grid");
+  }
+  return EIK_OK;
 }
 
 // per-row CSR for a sorted node list (validates order and bounds): rows of
@@ -832,8 +859,18 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
     const char* e = std::getenv("EIK_GRAPH");
     return !(e && e[0] == '0');
   }();
-  const bool graphable = graphs && !(flags & (EIK_HOST_INPUTS | EIK_HOST_OUTPUTS | EIK_SYNC | EIK_CHECK_UNDERFLOW |
-                                              EIK_PROFILE | EIK_SLAB_P2P)) &&
+  // a caller that is itself capturing (torch.cuda.graph, cudaStreamBeginCapture)
+  // records the eager launches into its own graph; the dense mask fill
+  // (sign nodes > N/8) allocates temporaries and is never captured
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) != cudaSuccess) {
+    cudaGetLastError();  // e.g. the legacy stream during another stream's global-mode capture
+    cap = cudaStreamCaptureStatusActive;
+  }
+  const bool dense_fill = out->mask && in->n_sign_nodes > p->N / 8;
+  const bool graphable = graphs && cap == cudaStreamCaptureStatusNone && !dense_fill &&
+                         !(flags & (EIK_HOST_INPUTS | EIK_HOST_OUTPUTS | EIK_SYNC | EIK_CHECK_UNDERFLOW |
+                                    EIK_PROFILE | EIK_SLAB_P2P)) &&
                          !out->n_underflow && !p->copies_pending;
   if (!graphable) return run_locked(p, in, out, flags, stream);
   unsigned char key[sizeof(p->gkey)];
@@ -915,6 +952,13 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
   const int64_t* d_snodes = in->sign_nodes;
   const double* d_sw = in->sign_weights;
   const int64_t Ks = in->n_sign_nodes;
+  if (B > 65535) return fail(EIK_EVALIDATION, "batch larger than 65535 items");
+  if (host_in) {
+    int rc0;
+    if (want_phi && (rc0 = host_check_nodes(in->nodes, in->n_nodes, B > 1 ? in->item_offsets : nullptr, B, p->N)))
+      return rc0;
+    if (want_sign && (rc0 = host_check_nodes(in->sign_nodes, Ks, nullptr, 1, p->N))) return rc0;
+  }
   if (want_phi && host_in) {
     CK(p->h_nodes.ensure(in->n_nodes * sizeof(int64_t)));
     CK(cudaMemcpyAsync(p->h_nodes.p, in->nodes, in->n_nodes * sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -976,6 +1020,13 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
   r.sign = want_sign;
   const int n_comp = r.n_comp();
   const int64_t ce = p->comp_elems();
+  // sign mask: every node classified by its own mu in the row epilogue, then
+  // the flagged (sign) nodes take their nearest unflagged node's class with
+  // scipy's EDT ties, as classify does (R/sign.py:179-195)
+  const bool want_fill = want_sign && out->mask;
+  const int64_t fill_counts[3] = {p->dim == 1 ? p->c[1] : p->c[0], p->c[1], p->c[2]};
+  if (want_fill) CK(p->fillbits.ensure(((p->N + 31) / 32) * sizeof(uint32_t)));
+  uint32_t* fbits = p->fillbits.as<uint32_t>();
   // EIK_WAVE=n (2-D distance batches on the row-DFT path): items run in waves
   // of n, column pass then row pass per wave, so the wave's T and U_j stay in
   // L2 between the passes instead of round-tripping HBM
@@ -1023,6 +1074,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       if (!want_sign) return EIK_OK;
       int rc2;
       if ((rc2 = mark(EIK_PASS_COL_SIGN, false))) return rc2;
+      if (want_fill && (rc2 = eik_fill_bits(d_snodes, Ks, p->N, fbits, ss))) return rc2;
       if ((rc2 = pass_col2d(p, true, d_snodes, nullptr, Ks, 1, d_sw, r, W.data(), ss))) return rc2;
       if ((rc2 = mark(EIK_PASS_COL_SIGN, true))) return rc2;
       if (fork) CK(cudaEventRecord(p->ev_join, ss));
@@ -1051,6 +1103,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     }
     if (want_sign) {
       if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
+      if (want_fill && (rc = eik_fill_bits(d_snodes, Ks, p->N, fbits, st))) return rc;
       if ((rc = pass_planes(p, true, d_snodes, nullptr, Ks, 1, d_sw, p->c[0], p->M[1], V, st)))
         return rc;
       if ((rc = pass_axis0(p, true, V, 0, p->M[1], 1, r, W.data(), st))) return rc;
@@ -1121,6 +1174,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       CK(cudaStreamWaitEvent(p->st_copy2, p->ev_chunk, 0));
       int k = 0;
       for (auto& sl : slots) {
+        if (want_fill && sl.user == out->mask) continue;  // copied after the fill
         const size_t elem = sl.bytes / (size_t)NB;
         for (int64_t it = i0; it < i1; ++it) {
           const size_t off = ((size_t)it * item_nodes + (size_t)r0 * nlast) * elem;
@@ -1132,6 +1186,13 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       return EIK_OK;
     };
     if ((rc = finish(on_chunk))) return rc;
+    if (want_fill) {
+      if ((rc = eik_fill_mask(p->dim, fill_counts, d_snodes, Ks, fbits, o_mask, st))) return rc;
+      CK(cudaEventRecord(p->ev_chunk, st));
+      CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
+      for (auto& sl : slots)
+        if (sl.user == out->mask) CK(cudaMemcpyAsync(sl.user, sl.dev, sl.bytes, cudaMemcpyDeviceToHost, p->st_copy));
+    }
     CK(cudaEventRecord(p->ev_chunk, p->st_copy2));
     CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
     CK(cudaEventRecord(p->ev_copies, p->st_copy));
@@ -1140,6 +1201,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     slots.clear();
   } else {
     if ((rc = finish(nullptr))) return rc;
+    if (want_fill && (rc = eik_fill_mask(p->dim, fill_counts, d_snodes, Ks, fbits, o_mask, st))) return rc;
   }
   // ---- copy back / sync / checks
   for (auto& s : slots) CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));
@@ -1344,6 +1406,16 @@ int eik_slab_finish(eik_plan* p, double* const* w, int64_t c0_local, int64_t ks,
   if ((rc = pass_finish(p, W.data(), r, c0_local, ks, 1, ra, st, nomark))) return rc;
   if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
   return EIK_OK;
+}
+
+int eik_slab_fill(eik_plan* p, const int64_t* ext_nodes, int64_t n_ext, int64_t e0, int64_t e1, int64_t own0,
+                  int64_t c0_local, const uint8_t* mask_ext, uint8_t* mask_own, void* stream) {
+  if (!p || (n_ext > 0 && (!ext_nodes || !mask_ext || !mask_own))) return fail(EIK_EVALIDATION, "null argument");
+  if (p->D != 3) return fail(EIK_EVALIDATION, "the slab API is for 3-D grids");
+  CK(cudaSetDevice(p->device));
+  const int64_t counts[3] = {p->c[0], p->c[1], p->c[2]};
+  return eik_slab_fill_mask(counts, ext_nodes, n_ext, e0, e1, own0, c0_local, mask_ext, mask_own,
+                            static_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------------------

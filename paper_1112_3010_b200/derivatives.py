@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
-from .distance import _UNDERFLOW_MSG, distinct_nodes
+from .distance import distinct_nodes, underflow_message
 from .errors import PrecisionError, ValidationError
 from .grid import ScalarField, VectorField
 from .precision import arithmetic
@@ -40,7 +40,7 @@ def gradient(ps, grid, cfg, method: str = "fft") -> VectorField:
     try:
         plan.run(nodes, grad=comps, check_underflow=True)
     except PrecisionError:
-        raise PrecisionError(_UNDERFLOW_MSG.format(what="gradient denominator")) from None
+        raise PrecisionError(underflow_message(mode, "gradient denominator")) from None
     return VectorField([ScalarField(grid, c, nodes) for c in comps])
 
 
@@ -57,7 +57,7 @@ def hessian_2d(ps, grid, cfg, method: str = "fft"):
     try:
         plan.run(nodes, hess=h, check_underflow=True)
     except PrecisionError:
-        raise PrecisionError(_UNDERFLOW_MSG.format(what="gradient denominator")) from None
+        raise PrecisionError(underflow_message(mode, "gradient denominator")) from None
     return tuple(ScalarField(grid, x, nodes) for x in h)
 
 

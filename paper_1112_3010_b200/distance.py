@@ -20,6 +20,16 @@ _UNDERFLOW_MSG = (
     "{what} has non-positive entries after convolution; increase the precision bits "
     "(e.g. --precision big:512) or raise tau"
 )
+# the double-double path keeps float64's exponent range, so more bits cannot
+# help it: only a larger tau does (this build runs big-float configs up to 106 bits)
+_DD_UNDERFLOW_MSG = (
+    "{what} has non-positive entries after the double-double (106-bit) convolution; its exponent "
+    "range is float64's, so raise tau (bigfloat precision above 106 bits is not available in this build)"
+)
+
+
+def underflow_message(mode: str, what: str) -> str:
+    return (_DD_UNDERFLOW_MSG if mode == "dd" else _UNDERFLOW_MSG).format(what=what)
 
 
 def distinct_nodes(ps, grid) -> np.ndarray:
@@ -69,7 +79,7 @@ def _run_phi_family(ps, grid, cfg, *, want_s: bool, what: str):
         try:
             plan.run(nodes, check_underflow=True, **kw)
         except PrecisionError:
-            raise PrecisionError(_UNDERFLOW_MSG.format(what=what)) from None
+            raise PrecisionError(underflow_message(mode, what)) from None
         return out
     plan = _native.get_plan(grid, tau, _native.FIELD_PHI | _native.FIELD_S)
     kw = {"S": out} if want_s else {"phi": out}
@@ -80,14 +90,37 @@ def _run_phi_family(ps, grid, cfg, *, want_s: bool, what: str):
     return out
 
 
+def _phi_from_kernel_hat(ps, grid, cfg, convolver, kernel_hat):
+    """The reuse branch of R/distance.py:82-84: g_hat = impulse_hat(g), then
+    inverse_to_grid(product(kernel_hat, g_hat)), on the device spectral API.
+    kernel_hat is the caller's spectrum of shape FftConvolver.pshape (the
+    reference's padded shape, so spectra from either package fit)."""
+    from .convolution import FftConvolver, assert_positive
+
+    require_native(cfg)
+    conv = convolver if isinstance(convolver, FftConvolver) else FftConvolver(grid, getattr(
+        convolver, "kshape", tuple(2 * c - 1 for c in grid.counts)), cfg)
+    g_hat = conv.impulse_hat(impulse_field(ps, grid))
+    values = conv.inverse_to_grid(conv.product(kernel_hat, g_hat)).reshape(-1)
+    try:
+        assert_positive(values, "phi")
+    except PrecisionError:
+        raise PrecisionError(_UNDERFLOW_MSG.format(what="phi")) from None
+    return values
+
+
 def phi_fft(ps, grid, cfg, convolver=None, kernel_hat=None) -> ScalarField:
     """phi = exp(-|x|/tau) * delta_Y on the grid; PrecisionError if any phi <= 0.
 
-    `convolver`/`kernel_hat` are accepted for signature compatibility; kernel
-    spectra are always reused through the plan cache (the reference's reuse hook).
-    For big-float configs phi comes from the double-double convolution and is
-    returned rounded to float64 (the reference returns mpfr objects).
+    Reuse hook (R/distance.py:63-86): without `kernel_hat` the exp kernel's
+    spectrum is reused through the plan cache (a passed `convolver` needs no
+    other state); with `convolver` and `kernel_hat` the given spectrum is
+    applied through the spectral API.  For big-float configs phi comes from the
+    double-double convolution and is returned rounded to float64 (the reference
+    returns mpfr objects).
     """
+    if convolver is not None and kernel_hat is not None:
+        return ScalarField(grid, _phi_from_kernel_hat(ps, grid, cfg, convolver, kernel_hat))
     return ScalarField(grid, _run_phi_family(ps, grid, cfg, want_s=False, what="phi"))
 
 
@@ -101,7 +134,10 @@ def s_from_phi(phi: ScalarField, cfg) -> ScalarField:
 
 
 def s_fft(ps, grid, cfg, convolver=None, kernel_hat=None) -> ScalarField:
-    """Composed pipeline (R/distance.py:114-122), fused on the device."""
+    """Composed pipeline (R/distance.py:114-122), fused on the device (the
+    kernel_hat reuse branch goes through phi_fft + s_from_phi as in the reference)."""
+    if convolver is not None and kernel_hat is not None:
+        return s_from_phi(phi_fft(ps, grid, cfg, convolver, kernel_hat), cfg)
     return ScalarField(grid, _run_phi_family(ps, grid, cfg, want_s=True, what="phi"))
 
 

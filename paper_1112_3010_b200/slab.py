@@ -84,6 +84,79 @@ def local_nodes(nodes, layout: SlabLayout, weights=None):
     return ln, np.ascontiguousarray(np.asarray(weights)[:, a:b])
 
 
+def halo_planes(layout: SlabLayout, hd: int):
+    """Planes [e0, e1): the rank's own planes plus up to hd neighbour planes each side."""
+    e0 = max(0, layout.i0_begin - hd)
+    e1 = min(layout.counts[0], layout.i0_begin + layout.c0loc + hd)
+    return e0, e1
+
+
+def ext_flagged(sign_nodes, layout: SlabLayout, hd: int):
+    """Flagged (sign) nodes of planes [e0, e1), flat relative to plane e0."""
+    e0, e1 = halo_planes(layout, hd)
+    nodes = np.asarray(sign_nodes, dtype=np.int64)
+    pl = layout.plane_nodes
+    a, b = np.searchsorted(nodes, [e0 * pl, e1 * pl])
+    return np.ascontiguousarray(nodes[a:b] - e0 * pl), e0, e1
+
+
+def fill_masks_emulated(executors, outs, sign_nodes, hd=8):
+    """Flagged-node fill of every emulated rank's mask (classify, R/sign.py:179-195):
+    each rank reads the neighbours' halo planes straight from their outputs."""
+    import torch
+
+    L0 = executors[0].layout
+    while True:
+        full = torch.cat([o["mask"].view(-1) for o in outs]).view(L0.counts[0], -1)
+        try:
+            for ex, o in zip(executors, outs):
+                ext, e0, e1 = ext_flagged(sign_nodes, ex.layout, hd)
+                ex.fill(o, ext, e0, e1, full[e0:e1].contiguous())
+            return outs
+        except ValidationError:
+            if hd >= L0.counts[0]:
+                raise
+            hd *= 2
+
+
+def fill_rank(ex, out, sign_nodes, dist, hd=8):
+    """Flagged-node fill of one rank's mask: halo planes of the mask from the
+    neighbouring ranks (point-to-point), then eik_slab_fill; the halo doubles,
+    on every rank at once, until no nearest-unflagged search leaves it."""
+    import torch
+
+    L = ex.layout
+    G, r = L.world, L.rank
+    mask = out["mask"].view(L.c0loc, -1)
+    # NCCL moves device tensors; other backends (gloo in the tests) host copies
+    wire = mask.device if dist.get_backend() == "nccl" else torch.device("cpu")
+    while True:
+        h = min(hd, L.c0loc)
+        ops = []
+        lo = torch.empty((h, mask.shape[1]), dtype=torch.uint8, device=wire) if r > 0 else None
+        hi = torch.empty((h, mask.shape[1]), dtype=torch.uint8, device=wire) if r < G - 1 else None
+        if r > 0:
+            ops += [dist.P2POp(dist.isend, mask[:h].contiguous().to(wire), r - 1), dist.P2POp(dist.irecv, lo, r - 1)]
+        if r < G - 1:
+            ops += [dist.P2POp(dist.isend, mask[-h:].contiguous().to(wire), r + 1), dist.P2POp(dist.irecv, hi, r + 1)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        parts = [x.to(mask.device) for x in (lo, mask, hi) if x is not None]
+        ext, e0, e1 = ext_flagged(sign_nodes, L, h)
+        ok = torch.ones(1, device=wire)
+        try:
+            ex.fill(out, ext, e0, e1, torch.cat(parts).contiguous())
+        except ValidationError:
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() > 0:
+            return out
+        if h >= L.c0loc:
+            raise ValidationError("slab fill: a nearest-unflagged search spans more than one neighbour slab")
+        hd *= 2
+
+
 def run_rank(ex, exchange, nodes, sign_nodes=None, sign_weights=None):
     """One rank of the slab schedule.  `nodes` etc. are this rank's local lists."""
     ex.planes(0, nodes, None)
@@ -271,6 +344,14 @@ class CudaSlabExecutor:
             return
         out = [self.W[self.n_dist]] if group else self.W[: self.n_dist]
         self.plan.slab_axis0(group, self.V_recv[:3 if group else 1], L.k1_begin, L.ks, out, self._stream())
+
+    def fill(self, out, ext_nodes, e0, e1, mask_ext):
+        """eik_slab_fill: the owned flagged nodes of out["mask"] from the halo-extended mask."""
+        import torch
+
+        nd = torch.as_tensor(np.ascontiguousarray(ext_nodes, dtype=np.int64), device=self.dev)
+        L = self.layout
+        self.plan.slab_fill(nd, e0, e1, L.i0_begin, L.c0loc, mask_ext, out["mask"], self._stream())
 
     def finish(self):
         import torch

@@ -432,3 +432,69 @@ def test_graph_replay_with_sign_group(cuda_ok):
         assert np.array_equal(mask.cpu().numpy(), ref["mask"]), i
         for a in range(3):
             assert np.array_equal(hess[a].cpu().numpy(), ref["hess"][a], equal_nan=True), i
+
+
+def test_caller_stream_capture(cuda_ok):
+    """A caller capturing its own stream (torch.cuda.graph) after warm-up calls
+    records eik_run's eager launches into its graph: replaying that graph
+    reproduces the eager result, including the sign mask fill."""
+    import torch
+
+    from paper_1112_3010_b200 import _native, engine, workloads
+
+    d = workloads.c2(seed=4, n=128, k=1024, radius=40.0, tau=1.0)
+    grid = d["grid"]
+    N = grid.num_nodes
+    dt = engine.DistanceTransform(grid, 1.0, grad=True, sign=True)
+    sn, sw = dt.sign_inputs(d["curve"])
+    nd = d["points"].distinct_nodes()
+    ref = dt.run_host(nd, sign_nodes=sn, sign_weights=sw)
+    plan = _native.Plan(2, grid.counts, grid.spacing, 1.0, engine.field_bits(2, True, False, True), 0)
+    dev = torch.device("cuda", 0)
+    nodes, snodes, sweights = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (nd, sn, sw))
+    S = torch.empty(N, dtype=torch.float64, device=dev)
+    mu = torch.empty_like(S)
+    grad = [torch.empty_like(S), torch.empty_like(S)]
+    mask = torch.empty(N, dtype=torch.uint8, device=dev)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        for _ in range(3):  # warm-up: the plan's own graph is captured at the second call
+            plan.run(nodes, None, 1, snodes, sweights, S=S, grad=grad, mu=mu, mask=mask, host=False,
+                     stream=side.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.run(nodes, None, 1, snodes, sweights, S=S, grad=grad, mu=mu, mask=mask, host=False,
+                 stream=torch.cuda.current_stream().cuda_stream)
+    for _ in range(2):
+        S.fill_(-1.0)
+        mask.fill_(7)
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(S.cpu().numpy(), ref["S"], equal_nan=True)
+        assert np.array_equal(mask.cpu().numpy(), ref["mask"])
+        assert np.array_equal(grad[1].cpu().numpy(), ref["grad"][1], equal_nan=True)
+
+
+def test_async_host_path_validates_inputs(cuda_ok):
+    """The asynchronous host path (EIK_ASYNC) rejects bad node lists and item
+    offsets before queueing anything (host-side checks)."""
+    import torch
+
+    from paper_1112_3010_b200 import ValidationError, engine
+
+    grid = _grid((64, 64))
+    dt = engine.DistanceTransform(grid, 20.0, grad=False)
+    S = torch.empty(grid.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
+    for bad in ([5, 3], [1, 1], [-1, 4], [0, grid.num_nodes]):
+        with pytest.raises(ValidationError):
+            dt.plan.run(np.array(bad, dtype=np.int64), S=S, host=True, wait=False)
+    S2 = torch.empty(2 * grid.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
+    for offs in ([0, 3, 2], [1, 2, 4], [0, 2, 3]):
+        with pytest.raises(ValidationError):
+            dt.plan.run(np.array([1, 5, 7, 9], dtype=np.int64), np.array(offs, dtype=np.int64), 2, S=S2,
+                        host=True, wait=False)
+    dt.plan.run(np.array([1, 5, 7, 9], dtype=np.int64), np.array([0, 2, 4], dtype=np.int64), 2, S=S2, host=True)
+    assert np.isfinite(S2).all()
+    with pytest.raises(ValidationError):
+        dt.plan.run(np.zeros(0, dtype=np.int64), np.zeros(65537, dtype=np.int64), 65536, S=S2, host=True)

@@ -15,7 +15,8 @@ def test_emulated_slab_bit_identical(cuda_ok, world, p2p):
     import torch
 
     from paper_1112_3010_b200 import GridSpec, engine, workloads
-    from paper_1112_3010_b200.slab import CudaSlabExecutor, local_nodes, run_emulated, run_emulated_p2p
+    from paper_1112_3010_b200.slab import (CudaSlabExecutor, fill_masks_emulated, local_nodes, run_emulated,
+                                           run_emulated_p2p)
 
     grid = GridSpec((-15.5, -15.5, -15.5), 1.0, (32, 32, 32))
     tau = 0.75
@@ -34,6 +35,7 @@ def test_emulated_slab_bit_identical(cuda_ok, world, p2p):
         lsn, lsw = local_nodes(sn, ex.layout, sw)
         lists.append((ln, lsn, lsw))
     outs = (run_emulated_p2p if p2p else run_emulated)(exs, lists)
+    fill_masks_emulated(exs, outs, sn, hd=1)
     torch.cuda.synchronize()
     got = {k: torch.cat([o[k] for o in outs]).cpu().numpy() for k in ("S", "mu", "mask")}
     for a in range(3):

@@ -42,7 +42,7 @@ def _worker(rank, world, port, outdir):
     import torch
     import torch.distributed as dist
 
-    from paper_1112_3010_b200.slab import CudaSlabExecutor, connect_p2p, local_nodes, run_rank_p2p
+    from paper_1112_3010_b200.slab import CudaSlabExecutor, connect_p2p, fill_rank, local_nodes, run_rank_p2p
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -59,6 +59,8 @@ def _worker(rank, world, port, outdir):
     lsn, lsw = local_nodes(sn, ex.layout, sw)
     for _ in range(2):  # two steps through the same arenas
         out = run_rank_p2p(ex, barrier, ln, lsn, lsw)
+    torch.cuda.synchronize()
+    fill_rank(ex, out, sn, dist, hd=1)  # mask halos over gloo (host copies); hd=1 exercises the widening
     torch.cuda.synchronize()
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), S=out["S"].cpu().numpy(), mu=out["mu"].cpu().numpy(),
              mask=out["mask"].cpu().numpy(), **{f"g{a}": out["grad"][a].cpu().numpy() for a in range(3)})
