@@ -55,7 +55,71 @@ def parse():
     ap.add_argument("--items", type=int, default=512, help="C5 batch size (whole job)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="C4 slab exchange: fused peer stores (p2p) or NCCL all_to_all_single")
+    ap.add_argument("--c4-size", type=int, default=0,
+                    help="C4 grid edge (default 1024 on >= 4 GPUs, else 512: one fixed size for a strong-scaling "
+                         "series, pass e.g. --c4-size 512 at every N)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no device work: launch the ranks (gloo), build each rank's shard and print the line "
+                         "skeleton (tests the multi-rank plumbing on CPU)")
     return ap.parse_args()
+
+
+# ---------------------------------------------------------------- ranks
+
+
+def spawn_ranks(a):
+    """`--gpus N` outside torchrun: re-launch this script with N local ranks
+    (torch.distributed.run, rendezvous on 127.0.0.1), return its exit code."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def rank_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def init_ranks(world, local, cpu_only=False):
+    """(dist | None, device index, oversubscribed).  NCCL when every rank has its
+    own GPU; gloo on CPU (dry runs, tests) or when ranks share a device (NCCL
+    cannot place two ranks on one GPU; such a run is a functional check only)."""
+    if world <= 1:
+        return None, local, False
+    import torch
+    import torch.distributed as dist
+
+    ndev = 0 if cpu_only or not torch.cuda.is_available() else torch.cuda.device_count()
+    over = ndev < world
+    if ndev and not over:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+    return dist, (local % ndev if ndev else local), over
+
+
+def reduce_max(dist, value, dev=None):
+    """Max over ranks (device tensor for NCCL, host tensor for gloo)."""
+    if dist is None:
+        return value
+    import torch
+
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def shard_items(items, rank, world):
+    """C5: rank r takes items [r*per, (r+1)*per), per = items // world (no data-path collective)."""
+    per = items // world
+    return rank * per, per
 
 
 # ---------------------------------------------------------------- workloads
@@ -77,8 +141,8 @@ def build_workload(cfg, seed, rank=0, world=1, items=512):
         d = wl.c3(seed)
         return dict(grid=d["grid"], tau=d["tau"], nodes=[d["points"].distinct_nodes()], grad=True)
     if cfg == "C5":
-        per = items // world
-        d = wl.c5(seed, items=per, first=rank * per)
+        first, per = shard_items(items, rank, world)
+        d = wl.c5(seed, items=per, first=first)
         return dict(grid=d["grid"], tau=d["tau"], nodes=[p.distinct_nodes() for p in d["items"]], grad=True,
                     items_total=per * world)
     raise ValueError(cfg)
@@ -228,15 +292,16 @@ def oracle_step(w):
             orc.gradient_unchecked(nodes, grid.counts, grid.spacing, w["tau"])
         pts += grid.num_nodes
     if w.get("curve") is not None:
-        orc.winding_field(w["curve"].vertices, grid.origin, grid.spacing, grid.counts)
+        mu, flagged = orc.winding_field(w["curve"].vertices, grid.origin, grid.spacing, grid.counts)
+        orc.classify(mu, flagged, grid.counts, "winding2d")  # the mask, flagged nodes filled (R/sign.py:166-198)
     return pts
 
 
-def cpu_time(w, steps, warmup, budget_s=None):
+def cpu_time(w, steps, warmup, budget_s=None, workers=None):
     import scipy.fft as sfft
 
     sys.path.insert(0, os.path.join(REPO, "oracle"))
-    cores = os.cpu_count() or 1
+    cores = workers or os.cpu_count() or 1
     with sfft.set_workers(cores):
         for _ in range(warmup):
             oracle_step(w)
@@ -255,15 +320,52 @@ def cpu_time(w, steps, warmup, budget_s=None):
 # ---------------------------------------------------------------- GPU side
 
 
+def parallelism(cfg, world, over=False):
+    p = {"C5": f"batch-shard x{world} (no data-path collective)", "C4": f"slab x{world}"}.get(
+        cfg, f"replicas x{world} (the grid does not shard)")
+    return p + (" [ranks share one device: functional check, not a scaling number]" if over else "")
+
+
+def dry_run(a):
+    """Rank plumbing without device work: every rank builds its shard; rank 0 prints the gathered layout."""
+    rank, world, local = rank_env()
+    dist, _, _ = init_ranks(world, local, cpu_only=True)
+    if a.config in ("C1", "C2", "C3", "C5"):
+        w = build_workload(a.config, a.seed, rank, world, a.items)
+        first = shard_items(a.items, rank, world)[0] if a.config == "C5" else 0
+        mine = {"rank": rank, "first_item": first, "items": len(w["nodes"]),
+                "nodes": int(sum(len(n) for n in w["nodes"])), "grid_points": len(w["nodes"]) * w["grid"].num_nodes}
+    else:
+        mine = {"rank": rank}
+    shards = [mine]
+    if dist:
+        shards = [None] * world
+        dist.all_gather_object(shards, mine)
+    slowest = reduce_max(dist, float(rank))
+    if rank == 0:
+        pts = sum(x.get("grid_points", 0) for x in shards)
+        print(json.dumps({"metric": "grid points/sec (S+grad S+sign)", "value": None, "unit": "grid_points/s",
+                          "n_gpus": world, "dry_run": True, "steps": 0, "warmup": 0,
+                          "scaling": "strong" if a.config in ("C4", "C5") else "weak",
+                          "config": {"workload": a.config, "desc": CONFIG_TEXT[a.config],
+                                     "parallelism": parallelism(a.config, world)},
+                          "grid_points_per_step_job": pts, "shards": shards, "max_over_ranks_check": slowest}))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(a)
+    if a.dry_run:
+        return dry_run(a)
     if a.config == "C4" and a.impl == "b200":
         return bench_c4(a)
     if a.config == "TS":
         return bench_sweep(a)
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    rank, world, local = rank_env()
     sys.path.insert(0, os.path.join(REPO, "oracle"))
 
     if a.impl == "reference":
@@ -278,6 +380,11 @@ def main():
             w["nodes"] = w["nodes"][:8]
         # CPU has no warm-up effects worth W full steps of a ~10 s pipeline; one is run
         val, sec, done, cores = cpu_time(w, a.steps, min(a.warmup, 1), budget_s=240.0)
+        # the reference as shipped: scipy.fft's default single worker, one step
+        # (the public calls raise PrecisionError on C2/C3/C5 only after all
+        # their transforms ran, R/convolution.py:378-388, so the unchecked
+        # pipeline takes the same time)
+        v1, sec1, _, _ = cpu_time(w, 1, 0, workers=1)
         line = {
             "metric": "grid points/sec (S+grad S+sign)", "value": val, "unit": "grid_points/s", "n_gpus": a.gpus,
             "steps": done, "warmup": min(a.warmup, 1), "ms_per_step": sec * 1e3, "higher_is_better": True,
@@ -289,17 +396,15 @@ def main():
                                        + (" (8 of 512 items per step)" if a.config == "C5" else "")
                                        + f", scipy.fft workers={cores}"},
             "e2e": {"value": val, "unit": "grid_points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "as_shipped": {"value": v1, "unit": "grid_points/s", "cores": 1, "ms_per_step": sec1 * 1e3,
+                           "sample": "1 step, scipy.fft workers=1 (the reference's default)"},
         }
         print(json.dumps(line))
         return 0
 
     import torch
 
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, local, over = init_ranks(world, local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1112_3010_b200 import _native
@@ -366,11 +471,8 @@ def main():
             ev[i][1].record(stream)
             clk.sample()  # host-side, while the step runs on the device
         torch.cuda.synchronize()
-    total_ms = sum(s.elapsed_time(e) for s, e in ev)
+    total_ms = reduce_max(dist, sum(s.elapsed_time(e) for s, e in ev), dev)
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
     pts_per_step_job = B * N * world
     value = pts_per_step_job * a.steps / (total_ms / 1e3)
@@ -408,10 +510,11 @@ def main():
         ho["hess"] = [pinned(B * N, torch.float64) for _ in range(3)]
         d2h += 3 * B * N * 8
     if sn_h is not None:
-        # the config's sign output is the inside/outside mask (classify's rint(mu) > 0);
-        # the winding number mu itself stays on the device in the e2e arm
+        # the sign outputs: the winding number mu and the interior mask (classify's
+        # rule with the flagged-node fill, R/sign.py:166-198)
+        ho["mu"] = pinned(N, torch.float64)
         ho["mask"] = pinned(N, torch.uint8)
-        d2h += N
+        d2h += 9 * N
     h2d = nodes_h.nbytes + (offs_h.nbytes if offs_h is not None else 16) + \
         ((sn_h.nbytes + sw_h.nbytes + 16) if sn_h is not None else 0)
 
@@ -435,11 +538,7 @@ def main():
         e2e_step(wait=(i == ke - 1))
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = reduce_max(dist, e0.elapsed_time(e1), dev)
     e2e_val = pts_per_step_job * ke / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant pass
@@ -483,9 +582,10 @@ def main():
                "sample": f"1 step of the oracle pipeline on {a.config}" + (" (8 items)" if a.config == "C5" else "")
                          + f" ({sec:.1f} s), scipy.fft workers={cores}"}
 
-    # kernels per step: per group prep_nodes + rowptr + impulse_rows + column pass;
-    # + row pass (3-D: + axis-1 lines before/after the axis-0 pass)
-    launches_per_step = {"C1": 4, "C2": 7, "C3": 6, "C5": 4}[a.config]  # prep_nodes, impulse rows, column, (lines), row per group
+    # kernels per step (profiles/round2 launch lists): per group prep_nodes +
+    # impulse_rows + column pass, then the row pass; C2 adds the sign mask fill
+    # (flag bitmap + per-flagged-node fix-up); 3-D adds the axis-1 lines passes
+    launches_per_step = {"C1": 4, "C2": 9, "C3": 6, "C5": 4}[a.config]
     if rank == 0:
         line = {
             "metric": "grid points/sec (S+grad S+sign)", "value": value, "unit": "grid_points/s", "n_gpus": world,
@@ -494,11 +594,11 @@ def main():
             "data": "synthetic (seeded generators of BASELINE.json configs, workloads.py)",
             "config": {"workload": a.config, "desc": CONFIG_TEXT[a.config], "grid": list(grid.counts),
                        "batch_per_rank": B, "padded": list(info["padded"]), "l2": "flushed between timed steps",
-                       "parallelism": "replicas" if a.config != "C5" else f"batch-shard x{world}",
+                       "parallelism": parallelism(a.config, world, over),
                        "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": e2e_val, "unit": "grid_points/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": ke,
-                    "outputs": [k for k in ("S", "grad", "hess", "mask") if k in ho]},
+                    "outputs": [k for k in ("S", "grad", "hess", "mu", "mask") if k in ho]},
             "gpu_launches": launches_per_step * a.steps,
             "pass_ms": {k: round(v, 5) for k, v in mean_pass.items()},
             "phi_validity": validity,
@@ -578,21 +678,15 @@ def bench_c4(a):
     """C4: slab-decomposed 3-D pipeline, one rank per GPU, NCCL all-to-all between passes."""
     import torch
 
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = rank_env()
+    dist, local, over = init_ranks(world, local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1112_3010_b200 import workloads as wl
-    from paper_1112_3010_b200.slab import (CudaSlabExecutor, connect_p2p, local_nodes, nccl_exchange, run_rank,
-                                           run_rank_p2p, stream_barrier)
+    from paper_1112_3010_b200.slab import (CudaSlabExecutor, connect_p2p, fill_masks_emulated, fill_rank,
+                                           local_nodes, nccl_exchange, run_rank, run_rank_p2p, stream_barrier)
 
-    n = 1024 if world >= 4 else 512
+    n = a.c4_size or (1024 if world >= 4 else 512)
     d = wl.c4(a.seed, n=n)
     grid = d["grid"]
     t_plan = time.perf_counter()
@@ -611,18 +705,32 @@ def bench_c4(a):
             ex.plan.slab_p2p_connect(peer_arenas=[ex.arena])
             barrier = lambda: None  # noqa: E731
 
-        def run_rank(ex_, _exchange, *args):
+        def run_p2p(ex_, _exchange, *args):
             return run_rank_p2p(ex_, barrier, *args)
+        run_schedule = run_p2p
         exchange = None
     elif dist:
+        run_schedule = run_rank
         exchange = nccl_exchange(dist)
     else:
+        run_schedule = run_rank
+
         def exchange(send, recv):
             for s_, r_ in zip(send, recv):
                 r_.copy_(s_)
+
+    def step(*args):
+        # the config's sign output is the classified mask: fill the flagged nodes
+        # from the neighbours' halo planes (classify, R/sign.py:166-198)
+        out_ = run_schedule(ex, exchange, *args)
+        if dist:
+            fill_rank(ex, out_, d["sign_nodes"], dist)
+        else:
+            fill_masks_emulated([ex], [out_], d["sign_nodes"])
+        return out_
     stream = torch.cuda.current_stream(dev)
     for _ in range(a.warmup):
-        run_rank(ex, exchange, ln_d, lsn_d, lsw_d)
+        step(ln_d, lsn_d, lsw_d)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -630,15 +738,11 @@ def bench_c4(a):
     with ClockSampler(local) as clk:
         for i in range(a.steps):
             ev[i][0].record(stream)
-            out = run_rank(ex, exchange, ln_d, lsn_d, lsw_d)
+            out = step(ln_d, lsn_d, lsw_d)
             ev[i][1].record(stream)
             clk.sample()
         torch.cuda.synchronize()
-    total_ms = sum(s_.elapsed_time(e_) for s_, e_ in ev)
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = reduce_max(dist, sum(s_.elapsed_time(e_) for s_, e_ in ev), dev)
     value = grid.num_nodes * a.steps / (total_ms / 1e3)
     # end to end: local node lists from host, the rank's fields back to pinned host memory
     host = {k: torch.empty(v.numel(), dtype=v.dtype, pin_memory=True) for k, v in
@@ -652,17 +756,13 @@ def bench_c4(a):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(ke):
-        o = run_rank(ex, exchange, ln, lsn, lsw)
+        o = step(ln, lsn, lsw)
         for k, v in host.items():
             src = o[k] if k in o else o["grad"][int(k[1])]
             v.copy_(src, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = reduce_max(dist, e0.elapsed_time(e1), dev)
     if rank == 0:
         L = ex.layout
         line = {
@@ -670,16 +770,17 @@ def bench_c4(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded perturbed icosphere, workloads.c4)",
-            "config": {"workload": "C4" if n == 1024 else "C4@512^3", "desc": CONFIG_TEXT["C4"], "grid": list(grid.counts),
+            "config": {"workload": "C4" if n == 1024 else f"C4@{n}^3", "desc": CONFIG_TEXT["C4"], "grid": list(grid.counts),
                        "padded": list(L.padded), "vertices": int(d["vertices"].shape[0]),
                        "nodes": int(d["nodes"].size),
-                       "parallelism": f"slab x{world} " + ("(exchange fused into the passes: NVLink peer stores, "
-                                                          "2 stream barriers)" if p2p else "(NCCL all-to-all)"),
+                       "parallelism": parallelism("C4", world, over) + (
+                           " (exchange fused into the passes: NVLink peer stores, 2 stream barriers; mask halo "
+                           "planes point-to-point)" if p2p else " (NCCL all-to-all)"),
                        "exchange_bytes_per_step": int(9 * 16 * L.buf * world * (world - 1) / world) if world > 1 else 0,
                        "l2": "working set >> L2", "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": grid.num_nodes * ke / (e2e_ms / 1e3), "unit": "grid_points/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": ke},
-            "gpu_launches": 10 * a.steps,
+            "gpu_launches": 12 * a.steps,
             "roofline": None,
             "cpu_baseline": {"value": None, "unit": "grid_points/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": "infeasible: the reference pads to 3072^3 (464 GB per complex array) and "

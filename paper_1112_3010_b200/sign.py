@@ -35,6 +35,12 @@ def _accumulate(idx: np.ndarray, weights: np.ndarray):
     return nodes, acc
 
 
+def _dense(grid, nodes, values):
+    g = np.zeros(grid.num_nodes)
+    g[nodes] = values
+    return ScalarField(grid, g)
+
+
 @dataclass(frozen=True)
 class TangentData:
     """Snapped chord tangents per vertex and their per-node sums (R/sign.py:34-57)."""
@@ -43,6 +49,7 @@ class TangentData:
     tangents: np.ndarray
     nodes: np.ndarray
     weights: np.ndarray  # (2, len(nodes))
+    grid: object = None
 
     @classmethod
     def build(cls, curve, grid) -> "TangentData":
@@ -52,7 +59,12 @@ class TangentData:
         snapped = grid.coords_of_flat(ps.snapped_indices)
         tangents = np.roll(snapped, -1, axis=0) - snapped
         nodes, w = _accumulate(ps.snapped_indices, tangents)
-        return cls(vertex_nodes=nodes, tangents=tangents, nodes=nodes, weights=w)
+        return cls(vertex_nodes=nodes, tangents=tangents, nodes=nodes, weights=w, grid=grid)
+
+    # the reference's dense impulse fields (R/sign.py:36-37), built on demand
+    # from the per-node sums (same values: np.add.at order)
+    g1 = property(lambda self: _dense(self.grid, self.nodes, self.weights[0]))
+    g2 = property(lambda self: _dense(self.grid, self.nodes, self.weights[1]))
 
 
 @dataclass(frozen=True)
@@ -62,6 +74,10 @@ class FluxData:
     center_nodes: np.ndarray
     nodes: np.ndarray
     weights: np.ndarray  # (3, len(nodes))
+    grid: object = None
+
+    # the reference's dense impulse fields (R/sign.py:64), built on demand
+    impulses = property(lambda self: tuple(_dense(self.grid, self.nodes, w) for w in self.weights))
 
     @classmethod
     def build(cls, surface, grid) -> "FluxData":
@@ -72,7 +88,7 @@ class FluxData:
         e2 = surface.triangles[:, 2] - surface.triangles[:, 0]
         areas = 0.5 * np.linalg.norm(np.cross(e1, e2), axis=1)
         nodes, w = _accumulate(ps.snapped_indices, surface.normals * areas[:, None])
-        return cls(center_nodes=nodes, nodes=nodes, weights=w)
+        return cls(center_nodes=nodes, nodes=nodes, weights=w, grid=grid)
 
 
 def _sign_run(grid, tau, field_bit, nodes, weights, want_mask=False):

@@ -80,7 +80,7 @@ def install():
 
     import eikfld_oracle as orc
     import paper_1112_3010_b200 as P
-    from paper_1112_3010_b200 import convolution, derivatives, distance, errors, grid, precision, sign
+    from paper_1112_3010_b200 import convolution, derivatives, distance, errors, experiments, grid, precision, sign
 
     sys.modules.setdefault("gmpy2", _gmpy2_stub())
     pkg = types.ModuleType("eikfld")
@@ -138,6 +138,7 @@ def install():
                               {"DirectionalKernels": DirectionalKernels, "gradient": gradient,
                                "hessian_2d": hessian_2d}),
         "sign": _clone("eikfld.sign", sign),
+        "experiments": _clone("eikfld.experiments", experiments),
     }
     sys.modules["eikfld"] = pkg
     for k, m in mods.items():
