@@ -167,8 +167,20 @@ __device__ __forceinline__ void bfly_levels(double2* x) {
 
 // In-register R-point DFT (natural order in/out), radix-2 DIT, R <= 16.
 // HALF_IN: a[R/2..R) are known zero (not read).
+// Timing-only debug switches (results are wrong with any of them on; used by
+// tools/ablate.sh to split a kernel's time into its FP64 / exchange / memory parts)
+#ifndef EIK_DBG_NODFT
+#define EIK_DBG_NODFT 0
+#endif
+#ifndef EIK_DBG_NOTW
+#define EIK_DBG_NOTW 0
+#endif
+#ifndef EIK_DBG_NOXCHG
+#define EIK_DBG_NOXCHG 0
+#endif
 template <int R, bool INV, bool HALF_IN>
 __device__ __forceinline__ void dft(double2* a) {
+  if constexpr (EIK_DBG_NODFT) return;
   if constexpr (R > 1) {
     double2 x[R];
     perm_load<R, 0, HALF_IN>(x, a);
@@ -498,6 +510,7 @@ struct Line4K {
 // v[r] *= W_4096^{t r} (or its conjugate), r = 1..15: TMEM cache or quarter table
 template <bool INV>
 __device__ __forceinline__ void f4k_twiddle_t(double2 (&v)[16], int t, const TwSrc& tw) {
+  if constexpr (EIK_DBG_NOTW) return;
   if (tw.tm) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -527,6 +540,7 @@ __device__ __forceinline__ void f4k_twiddle_t(double2 (&v)[16], int t, const TwS
 // v[r] *= W_256^{x r} (or conjugate), x = t & 15, from the stage table
 template <bool INV>
 __device__ __forceinline__ void f4k_twiddle_row(double2 (&v)[16], int x, const TwSrc& tw) {
+  if constexpr (EIK_DBG_NOTW) return;
   const double2* row = tw.st + x * 15 - 1;
 #pragma unroll
   for (int r = 1; r < 16; ++r) v[r] = INV ? cmulc(v[r], row[r]) : cmul(v[r], row[r]);
@@ -542,20 +556,24 @@ __device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& x
   double2* row = sm + g * P;
   dft<16, false, HALF_IN>(v);  // over n1: v[k1], thread t = n2
   f4k_twiddle_t<false>(v, t, tw);
+  if constexpr (!EIK_DBG_NOXCHG) {
   xb.sync();  // every thread is done with the buffer (previous transform)
 #pragma unroll
   for (int r = 0; r < 16; ++r) sm[r * P + t] = v[r];
   xb.sync();
 #pragma unroll
   for (int m = 0; m < 16; ++m) v[m] = row[x + 16 * m];  // row k1 = g, n2 = x + 16 m
+  }
   dft<16, false, false>(v);                             // over m: v[a], lane x = j
   f4k_twiddle_row<false>(v, x, tw);
+  if constexpr (!EIK_DBG_NOXCHG) {
   __syncwarp();
 #pragma unroll
   for (int a = 0; a < 16; ++a) row[a * 17 + x] = v[a];
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = row[x * 17 + j];  // lane x = a
+  }
   dft<16, false, false>(v);                             // over j: v[b] = X[g + 16 x + 256 b]
 }
 
@@ -567,13 +585,16 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& x
   double2* row = sm + g * P;
   dft<16, true, false>(v);  // over b: v[j], lane x = a
   f4k_twiddle_row<true>(v, x, tw);
+  if constexpr (!EIK_DBG_NOXCHG) {
   __syncwarp();  // the row is only touched by this half-warp since the last CTA barrier
 #pragma unroll
   for (int j = 0; j < 16; ++j) row[x * 17 + j] = v[j];
   __syncwarp();
 #pragma unroll
   for (int a = 0; a < 16; ++a) v[a] = row[a * 17 + x];  // lane x = j
+  }
   dft<16, true, false>(v);                              // over a: v[m] = z[x + 16 m]
+  if constexpr (!EIK_DBG_NOXCHG) {
   __syncwarp();
 #pragma unroll
   for (int m = 0; m < 16; ++m) row[x + 16 * m] = v[m];
@@ -581,6 +602,7 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& x
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = sm[r * P + t];  // thread t = n2: v[k1]
   xb.sync();  // buffer free again: the next transform may write any row
+  }
   f4k_twiddle_t<true>(v, t, tw);
   dft<16, true, false>(v);  // over k1: v[i] = x[t + 256 i]
 }

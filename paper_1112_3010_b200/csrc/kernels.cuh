@@ -541,18 +541,33 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_TSTORE
 #define EIK_TSTORE 0
 #endif
+// EIK_TM_E = 8: the TMEM column kernels of 1024- to 4096-point lines hold 8
+// values per thread (radix-8 Stockham stages) at twice the threads and half the
+// registers (64), i.e. 32 resident warps per SM instead of 16 (A/B switch).
+#ifndef EIK_TM_E
+#define EIK_TM_E 16
+#endif
+#ifndef EIK_TM_E8_MAXL
+#define EIK_TM_E8_MAXL 12
+#endif
+#ifndef EIK_TM_E8_MINL
+#define EIK_TM_E8_MINL 10
+#endif
 template <int L, int LPCX = 1>
 struct TmCfg {
-  static constexpr int TPL0 = tpl_of(L, 16);
-  static constexpr bool F4K = (L == 12 && EIK_FOUR_STEP);
-  static constexpr int NT = F4K ? 256 * LPCX : (TPL0 > 256 ? TPL0 : 256);
+  static constexpr int E = (EIK_TM_E == 8 && L >= EIK_TM_E8_MINL && L <= EIK_TM_E8_MAXL) ? 8 : 16;
+  static constexpr int TPL0 = tpl_of(L, E);
+  static constexpr bool F4K = (L == 12 && EIK_FOUR_STEP && E == 16);
+  static constexpr int NT = F4K ? 256 * LPCX : E == 8 ? (L >= 12 ? 1024 : 512) : (TPL0 > 256 ? TPL0 : 256);
   static constexpr int LPC = NT / TPL0;
-  static constexpr int MINB = NT >= 512 ? 1 : 2;
+  static constexpr int MINB = E == 8 ? (NT >= 1024 ? 1 : 2) : (NT >= 512 ? 1 : 2);
   // four-step lines: EIK_F4K_IL = 1 makes the CTA line-major (warps 0-7 line 0,
   // 8-15 line 1) with one named barrier per line, so the lines drift apart and
   // one line's FP64 phase can overlap the other's exchange
   static constexpr int IL = F4K ? (EIK_F4K_IL < LPC ? EIK_F4K_IL : LPC) : col_il(LPC);
-  using LN = std::conditional_t<F4K, Line4K, PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>;
+  using LN = std::conditional_t<F4K, Line4K,
+                                std::conditional_t<E == 8, PaddedLine<L, 8, col_pad(L, IL == 2 && LPC > 2)>,
+                                                   PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>>;
   using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
@@ -568,7 +583,7 @@ struct TmCfg {
   static constexpr int WPT = 4 * LN::EPT;  // 32-bit TMEM words per thread (forward spectrum)
   // 4096-point lines: the radix-16 NS=256 stage's twiddles W^{t r} are per-thread
   // constants shared by the forward and every inverse -> cached in TMEM too
-  static constexpr bool TWC = EIK_TWC && (L == 12) && LN::INV_SHARES;
+  static constexpr bool TWC = EIK_TWC && (L == 12) && LN::INV_SHARES && E == 16;
   // other long lines: the last inverse stage (radix R0 < 16 over NS = M/R0 > 16,
   // quarter-table twiddles otherwise) reads per-thread constants from TMEM
   // (C5 column kernel 5.19 -> 5.01 ms)
@@ -897,11 +912,17 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   }
   // kernel spectra: the next component's lines are prefetched into L1 one
   // transform ahead (no registers held across the FFT); loaded at use
-  if (valid) kprefetch_all<TC>(a.ks[0], l, t);
+#ifndef EIK_DBG_NOK
+#define EIK_DBG_NOK 0
+#endif
+#ifndef EIK_DBG_NOST
+#define EIK_DBG_NOST 0
+#endif
+  if (valid && !EIK_DBG_NOK) kprefetch_all<TC>(a.ks[0], l, t);
 #pragma unroll 1
   for (int j = 0; j < a.n_comp; ++j) {
     tmem_get(ta, v);
-    if (valid) {
+    if (valid && !EIK_DBG_NOK) {
       double kn[LN::EPT];
       kload_all<TC>(kn, a.ks[j], l, t);
       if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], l, t);
@@ -928,7 +949,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     for (int r = 0; r < LN::EPT; ++r) {
       if (LN::L > 0 && LN::upper_in(r)) continue;
       const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = v[r];
+      if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) *comp_dst(a, j, item, l, n) = v[r];
     }
   }
   tmem_free_cta(tbase, TC::COLS);

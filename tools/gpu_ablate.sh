@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/ablate; mkdir -p $O
+echo "== default"; bash tools/quick_bench.sh C2 2>&1 | tee $O/default.log
+for d in altv/*/; do v=$(basename $d); echo "== $v"; EIK_LIB=$PWD/altv/$v/libeikfld_b200.so bash tools/quick_bench.sh C2 2>&1 | tee $O/$v.log; done
