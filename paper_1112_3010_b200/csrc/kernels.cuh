@@ -177,6 +177,7 @@ struct KSpec {
   int64_t ld;
   int imag;
   int odd0;
+  int odd1;  // 3-D: odd along axis 1 (sign of the k1-mirrored lines, see ColArgs::fold_H)
   // Optional register-order copy (real/imaginary spectra, 2-D plans): the value
   // register r of thread tid of CTA tile b needs, at perm[(b * EPT + r) * NT + tid],
   // unfolded with the axis-0 parity sign applied.  Warp loads are contiguous
@@ -216,10 +217,17 @@ struct ColArgs {
   int64_t spec_ld;
   const double2* tw;
   int lmax;
-  int kfeed;  // set by the launcher: shared-memory feed of register-order kernel spectra
-  int tstore; // set by the launcher: component outputs leave through shared memory + TMA (umap[j])
-  CUtensorMap umap[MAXC];  // [item][row][2 * nlines doubles] view of out[j] (box: 2 LPC doubles x 256 rows)
-  int sfeed;  // set by the launcher: asynchronous shared-memory staging of the next dense input (SUM)
+  // persistent TMEM column kernels (set by the launcher): tiles of LPC lines per item, items
+  int64_t tiles, items;
+  // 3-D kernel spectra are stored folded along axis 1 (every kernel is even or
+  // odd there): line l = (k1 - fold_k1base) * fold_H + k2 of the pass reads the
+  // stored line (min(k1, M1 - k1) - fold_f0) * fold_H + k2, negated for odd
+  // kernels when k1 > M1/2.  fold_H = 0: lines are read as they are (2-D).
+  int fold_H, fold_M1;
+  int64_t fold_k1base, fold_f0;
+  // OUT_COMPS: add the component into its destination instead of overwriting it
+  // (streamed 3-D sign group: one flux input at a time, W += IFFT0(K_i FFT0(V_i)))
+  int accum;
   // Peer-block outputs (slab exchange fused into the pass, P2P over NVLink):
   // when blk[0] is set, output row n of component j is written to
   // blk[n >> blk_shift] + j * blk_cstride + item * out_item + (n mod 2^blk_shift) * out_es + l,
@@ -246,6 +254,16 @@ __device__ __forceinline__ double2 kmul(double2 x, const KSpec& k, int64_t l, in
   return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
 }
 
+// Stored kernel-spectrum line of pass line l (ColArgs::fold_H) and whether it is a k1 mirror.
+__device__ __forceinline__ int64_t fold_line(const ColArgs& a, int64_t l, bool& mir) {
+  mir = false;
+  if (!a.fold_H) return l;
+  const int64_t q = l / a.fold_H;
+  const int64_t k1 = a.fold_k1base + q;
+  mir = k1 > (a.fold_M1 >> 1);
+  return ((mir ? a.fold_M1 - k1 : k1) - a.fold_f0) * a.fold_H + (l - q * a.fold_H);
+}
+
 // Raw folded kernel spectrum value at (k0, l); the fold sign is applied at use
 // time (kapply) so a prefetch issued one FFT ahead does not stall on the load.
 __device__ __forceinline__ double kload(const KSpec& k, int64_t l, int k0, int M0) {
@@ -269,12 +287,12 @@ __device__ __forceinline__ void perm_thread(int& tc, int& rev) {
   }
 }
 template <class CFG>
-__device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpec& k, int64_t l, int t) {
+__device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpec& k, int64_t l, int t, int64_t bx) {
   using LN = typename CFG::LN;
   if (k.perm) {
     int tc, rev;
     perm_thread<CFG>(tc, rev);
-    const double* __restrict__ src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NTP + tc;
+    const double* __restrict__ src = k.perm + bx * LN::EPT * CFG::NTP + tc;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) kn[r] = __ldg(src + (rev ? LN::EPT - 1 - r : r) * CFG::NTP);
   } else {
@@ -288,12 +306,12 @@ __device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpe
 #endif
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 template <class CFG>
-__device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t) {
+__device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t, int64_t bx) {
   using LN = typename CFG::LN;
   if (k.perm) {
     int tc, rev;
     perm_thread<CFG>(tc, rev);
-    const double* src = k.perm + (int64_t)blockIdx.x * LN::EPT * CFG::NTP + tc;
+    const double* src = k.perm + bx * LN::EPT * CFG::NTP + tc;
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r) prefetch_l1(src + r * CFG::NTP);
   } else {
@@ -309,7 +327,12 @@ __device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t) 
 // sign cases are uniform per kernel, so they are branched on once, not selected
 // per element.
 template <class LN>
-__device__ __forceinline__ void kapply_all(double2 (&v)[LN::EPT], double (&kv)[LN::EPT], const KSpec& k, int t) {
+__device__ __forceinline__ void kapply_all(double2 (&v)[LN::EPT], double (&kv)[LN::EPT], const KSpec& k, int t,
+                                           bool mir = false) {
+  if (k.odd1 && mir) {
+#pragma unroll
+    for (int r = 0; r < LN::EPT; ++r) kv[r] = -kv[r];
+  }
   if (k.odd0) {
 #pragma unroll
     for (int r = 0; r < LN::EPT; ++r)
@@ -323,8 +346,8 @@ __device__ __forceinline__ void kapply_all(double2 (&v)[LN::EPT], double (&kv)[L
     for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(v[r].x * kv[r], v[r].y * kv[r]);
   }
 }
-__device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0) {
-  if (k.odd0 && k0 > (M0 >> 1)) v = -v;
+__device__ __forceinline__ double2 kapply(double2 x, double v, const KSpec& k, int k0, int M0, bool mir = false) {
+  if ((k.odd0 && k0 > (M0 >> 1)) != (k.odd1 && mir)) v = -v;
   return k.imag ? make_double2(-x.y * v, x.x * v) : make_double2(x.x * v, x.y * v);
 }
 
@@ -421,18 +444,21 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
     fft_line<LN, false, HALF>(v, t, xb, tws);
     const bool real_ks = a.ks[0].cplx == nullptr;
+    bool mir;
+    const int64_t lk = fold_line(a, l, mir);
     double kn[LN::EPT];  // next component's kernel spectrum, prefetched
     if (real_ks && valid) {
-      kload_all<ColCfg<L>>(kn, a.ks[0], l, t);
+      kload_all<ColCfg<L>>(kn, a.ks[0], lk, t, blockIdx.x);
     }
 #pragma unroll 1
     for (int j = 0; j < a.n_comp; ++j) {
       double2 y[LN::EPT];
       if (real_ks) {
 #pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) y[r] = valid ? kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M) : v[r];
+        for (int r = 0; r < LN::EPT; ++r)
+          y[r] = valid ? kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M, mir) : v[r];
         if (j + 1 < a.n_comp && valid) {
-          kload_all<ColCfg<L>>(kn, a.ks[j + 1], l, t);
+          kload_all<ColCfg<L>>(kn, a.ks[j + 1], lk, t, blockIdx.x);
         }
       } else {
 #pragma unroll
@@ -443,7 +469,10 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       for (int r = 0; r < LN::EPT; ++r) {
         if (LN::L > 0 && LN::upper_in(r)) continue;
         const int n = LN::in_idx(t, r);
-        if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = y[r];
+        if (valid && n < a.n_out) {
+          double2* dst = comp_dst(a, j, item, l, n);
+          *dst = a.accum ? cadd(*dst, y[r]) : y[r];
+        }
       }
     }
   } else if constexpr (OUT == OUT_SUM) {
@@ -453,9 +482,11 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 #pragma unroll 1
     for (int i = 0; i < a.n_in; ++i) {
       const bool real_ks = a.ks[i].cplx == nullptr;
+      bool mir;
+      const int64_t lk = fold_line(a, l, mir);
       double kn[LN::EPT];  // this input's kernel spectrum, loaded before its transform
       if (real_ks && valid) {
-        kload_all<ColCfg<L>>(kn, a.ks[i], l, t);
+        kload_all<ColCfg<L>>(kn, a.ks[i], lk, t, blockIdx.x);
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
@@ -463,7 +494,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       if (valid) {
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r)
-          y[r] = cadd(y[r], real_ks ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M)
+          y[r] = cadd(y[r], real_ks ? kapply(v[r], kn[r], a.ks[i], LN::out_idx(t, r), LN::M, mir)
                                     : kmul(v[r], a.ks[i], l, LN::out_idx(t, r), LN::M));
       }
     }
@@ -517,12 +548,6 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
 __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
   return (L == 12 && EIK_FOUR_STEP) ? (OUT == OUT_COMPS ? EIK_F4K_LPC : OUT == OUT_SUM ? EIK_F4K_LPC_SUM : 1) : 1;
 }
-#ifndef EIK_KFEED
-#define EIK_KFEED 0
-#endif
-#ifndef EIK_SFEED
-#define EIK_SFEED 0
-#endif
 #ifndef EIK_SPF
 #define EIK_SPF 1
 #endif
@@ -537,9 +562,6 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #endif
 #ifndef EIK_F4K_IL
 #define EIK_F4K_IL 2
-#endif
-#ifndef EIK_TSTORE
-#define EIK_TSTORE 0
 #endif
 // EIK_TM_E = 8: the TMEM column kernels of 1024- to 4096-point lines hold 8
 // values per thread (radix-8 Stockham stages) at twice the threads and half the
@@ -597,25 +619,6 @@ struct TmCfg {
   static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
-  // Kernel-spectrum feed (register-order spectra, 2-D plans): the CTA's whole
-  // block of the next component's spectrum (EPT x NT doubles, contiguous) is
-  // bulk-copied into shared memory one transform ahead, where it fits next to
-  // MINB resident CTAs (C2: 64 KB on top of 158 KB, one CTA per SM).
-  static constexpr size_t KFEED_BYTES = (size_t)LN::EPT * NT * sizeof(double);
-  static constexpr bool KFEED = EIK_KFEED && !PFOLD && (SMEM_BYTES + 16 + KFEED_BYTES) * MINB <= 227 * 1024;
-  static constexpr size_t SMEM_FEED_BYTES = SMEM_BYTES + (KFEED ? 16 + KFEED_BYTES : 0);
-  // SUM kernels (sign group): the next input line (half-padded: EPT/2 values
-  // per thread, thread-private slots) is staged with cp.async while the
-  // current input is transformed (C2: 64 KB next to 158 KB, one CTA per SM)
-  // TMA output stores (four-step lines, 2-D distance group): the component's
-  // output tile [M/2 rows][LPC lines] is staged in shared memory and leaves as
-  // 256-row TMA boxes instead of one 16-line global request per warp store
-  static constexpr size_t TSTORE_OFF = (SMEM_BYTES + 127) & ~size_t(127);  // TMA smem boxes: 128-byte aligned
-  static constexpr size_t TSTORE_BYTES = TSTORE_OFF - SMEM_BYTES + (size_t)(LN::M / 2) * LPC * sizeof(double2) + 128;
-  static constexpr bool TSTORE = EIK_TSTORE && F4K && LPC >= 2 && (SMEM_BYTES + TSTORE_BYTES) * MINB <= 227 * 1024;
-  static constexpr size_t SFEED_BYTES = (size_t)(LN::EPT / 2) * NT * sizeof(double2);
-  static constexpr bool SFEED = EIK_SFEED && (SMEM_BYTES + SFEED_BYTES) * MINB <= 227 * 1024;
-  static constexpr size_t SMEM_SFEED_BYTES = SMEM_BYTES + (SFEED ? SFEED_BYTES : 0);
 };
 
 // L2 prefetch for the CTA that runs one resident wave later (linear CTA index
@@ -697,6 +700,20 @@ __device__ __forceinline__ void unstage_dense(double2 (&v)[LN::EPT], const doubl
   }
 }
 
+// Persistent: the grid is at most one resident wave of CTAs (launch_tmem_t);
+// each CTA fills its twiddle tables, allocates its TMEM columns and caches its
+// per-thread twiddles once, then walks the (item, tile) list with stride
+// gridDim.x, tile index fastest, so concurrently running CTAs work on adjacent
+// columns.  a.tiles = tiles per item, a.items = items.
+#ifndef EIK_NEXTPF
+#define EIK_NEXTPF 0  // next-tile L2 prefetch: measured C2 col 0.361 -> 0.369 ms, C5 5.36 -> 5.48, C3 1.95 -> 2.03
+#endif
+#ifndef EIK_DBG_NOK
+#define EIK_DBG_NOK 0
+#endif
+#ifndef EIK_DBG_NOST
+#define EIK_DBG_NOST 0
+#endif
 template <int L, int IN, int OUT, bool HALF>
 __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpcx(L, OUT)>::MINB)
     col_tmem_kernel(const __grid_constant__ ColArgs a) {
@@ -706,22 +723,12 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   extern __shared__ double2 smem[];
   const int line = TC::line_of(threadIdx.x);
   const int t = TC::t_of(threadIdx.x);
-  const int64_t l = (int64_t)blockIdx.x * LPC + line;
-  const bool valid = l < a.nlines;
-  const int64_t item = blockIdx.y;
   typename TC::XB xb{smem + line * LN::SMEM, nullptr, 0, 1 + line / TC::IL};
   double2* twq = smem + LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
   uint32_t* slot = reinterpret_cast<uint32_t*>(sts + LN::ST_SIZE);
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
-  if (TC::KFEED && a.kfeed && OUT == OUT_COMPS && threadIdx.x == 0) {
-    mbar_init(reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if constexpr (EIK_L2PF && IN == IN_DENSE) {
-    if (a.din_item > 0 && !a.blk[0]) prefetch_dense_tile<LPC, TC::NT>(a, OUT == OUT_SUM ? a.n_in : 1, 148 * TC::MINB);
-  }
   const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle tables
   const uint32_t ta = tmem_thread_addr(tbase, TC::WPT_ALL);
   uint32_t ttw = 0;
@@ -739,217 +746,95 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
     tw_last_inv_fill<LN>(ttw2, t, twq, L);
   }
   const TwSrc tws{sts, twq, L, ttw, ttw2};
+  const int tiles = (int)a.tiles;
+  const int total = tiles * (int)a.items;  // < 2^31 (launcher)
 
-  double2 v[LN::EPT];
-  if constexpr (OUT == OUT_SUM) {
-    // y = sum_i K_i X_i accumulated in TMEM while each input is transformed in registers
-    constexpr bool SF = TC::SFEED && HALF && IN == IN_DENSE;
-    double2* sbuf = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES);
-    const bool sfeed = SF && a.sfeed;
 #pragma unroll 1
-    for (int i = 0; i < a.n_in; ++i) {
-#if EIK_KPF
-      if (valid) kprefetch_all<TC>(a.ks[i], l, t);  // into L1 while the input is transformed
-#else
-      double kn[LN::EPT];
-      if (valid) {
-        kload_all<TC>(kn, a.ks[i], l, t);
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int item = tile / tiles;
+    const int bx = tile - item * tiles;
+    const int64_t l = (int64_t)bx * LPC + line;
+    const bool valid = l < a.nlines;
+    bool mir;
+    const int64_t lk = fold_line(a, l, mir);
+    // the tile this CTA runs next: its dense input lines head for L2 meanwhile
+    auto next_prefetch = [&]() {
+      if constexpr (EIK_NEXTPF && IN == IN_DENSE) {
+        const int ntile = tile + gridDim.x;
+        if (ntile < total) {
+          const int nitem = ntile / tiles;
+          const int64_t nl = (int64_t)(ntile - nitem * tiles) * LPC + line;
+          if (nl < a.nlines) prefetch_dense_l2<LN, HALF>(a, t, nl, nitem, 0, true);
+        }
       }
-#endif
-      if constexpr (IN == IN_SPARSE) {
-        load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
-      } else if constexpr (SF) {
-        if (sfeed && i > 0) unstage_dense<LN, TC::NT>(v, sbuf);
-        else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-        // the next input lands in this thread's slots while this one is transformed
-        // (input 1 at once; later ones once this input's slots have been read)
-        if (sfeed && i == 0 && a.n_in > 1) stage_dense_async<LN, TC::NT>(sbuf, a, t, l, item, 1, valid);
-      } else {
-        load_dense<LN, HALF>(v, a, t, l, item, i, valid);
-        // the next input's line heads for L2 while this one is transformed
-        if (EIK_SPF && i + 1 < a.n_in) prefetch_dense_l2<LN, HALF>(a, t, l, item, i + 1, valid);
-      }
-      fft_line<LN, false, HALF>(v, t, xb, tws);
-      if constexpr (SF) {
-        if (sfeed && i >= 1 && i + 1 < a.n_in) stage_dense_async<LN, TC::NT>(sbuf, a, t, l, item, i + 1, valid);
-      }
-#if EIK_KPF
-      double kn[LN::EPT];
-      if (valid) kload_all<TC>(kn, a.ks[i], l, t);
-#endif
-      if (valid) {
-        kapply_all<LN>(v, kn, a.ks[i], t);
-      } else {
-#pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(0.0, 0.0);
-      }
-      if (i > 0) {
-        double2 y[LN::EPT];
-        tmem_get(ta, y);
-#pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) v[r] = cadd(y[r], v[r]);
-      }
-      if (i + 1 < a.n_in) tmem_put(ta, v);
-    }
-    fft_line<LN, true>(v, t, xb, tws);
-#pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) {
-      if (LN::L > 0 && LN::upper_in(r)) continue;
-      const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out) *comp_dst(a, 0, item, l, n) = v[r];
-    }
-    tmem_free_cta(tbase, TC::COLS);
-    return;
-  }
-  // kernel-spectrum feed (TC::KFEED, launched with a.kfeed): bar + buffer after the base layout
-  uint64_t* kbar = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + TC::SMEM_BYTES);
-  double* kbuf = reinterpret_cast<double*>(kbar + 2);
-  const bool kfeed = TC::KFEED && a.kfeed;
-  auto kfeed_issue = [&](int j) {
-    if (threadIdx.x == 0) {
-      fence_proxy_async_smem();
-      mbar_expect_tx(kbar, (uint32_t)TC::KFEED_BYTES);
-      bulk_g2s(kbuf, a.ks[j].perm + (int64_t)blockIdx.x * LN::EPT * TC::NT, (uint32_t)TC::KFEED_BYTES, kbar);
-    }
-  };
-  if (kfeed) kfeed_issue(0);  // lands while the input line is loaded and transformed
-  if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
-  else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
-  fft_line<LN, false, HALF>(v, t, xb, tws);
-  tmem_put(ta, v);
-  if (kfeed) {
+    };
+    double2 v[LN::EPT];
+    if constexpr (OUT == OUT_SUM) {
+      // y = sum_i K_i X_i accumulated in TMEM while each input is transformed in registers
 #pragma unroll 1
-    for (int j = 0; j < a.n_comp; ++j) {
-      tmem_get(ta, v);
-      double kn[LN::EPT];
-      mbar_wait(kbar, (uint32_t)(j & 1));
+      for (int i = 0; i < a.n_in; ++i) {
+        if (valid) kprefetch_all<TC>(a.ks[i], lk, t, bx);  // into L1 while the input is transformed
+        if constexpr (IN == IN_SPARSE) {
+          load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
+        } else {
+          load_dense<LN, HALF>(v, a, t, l, item, i, valid);
+          // the next input's line heads for L2 while this one is transformed
+          if (EIK_SPF && i + 1 < a.n_in) prefetch_dense_l2<LN, HALF>(a, t, l, item, i + 1, valid);
+          if (i + 1 == a.n_in) next_prefetch();
+        }
+        fft_line<LN, false, HALF>(v, t, xb, tws);
+        double kn[LN::EPT];
+        if (valid) {
+          kload_all<TC>(kn, a.ks[i], lk, t, bx);
+          kapply_all<LN>(v, kn, a.ks[i], t, mir);
+        } else {
 #pragma unroll
-      for (int r = 0; r < LN::EPT; ++r) kn[r] = kbuf[r * TC::NT + threadIdx.x];
-      __syncthreads();  // every thread has its values: the buffer may be refilled
-      if (j + 1 < a.n_comp) kfeed_issue(j + 1);
-      if (valid) kapply_all<LN>(v, kn, a.ks[j], t);
+          for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(0.0, 0.0);
+        }
+        if (i > 0) {
+          double2 y[LN::EPT];
+          tmem_get(ta, y);
+#pragma unroll
+          for (int r = 0; r < LN::EPT; ++r) v[r] = cadd(y[r], v[r]);
+        }
+        if (i + 1 < a.n_in) tmem_put(ta, v);
+      }
       fft_line<LN, true>(v, t, xb, tws);
 #pragma unroll
       for (int r = 0; r < LN::EPT; ++r) {
         if (LN::L > 0 && LN::upper_in(r)) continue;
         const int n = LN::in_idx(t, r);
-        if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = v[r];
+        if (valid && n < a.n_out) *comp_dst(a, 0, item, l, n) = v[r];
       }
-    }
-    tmem_free_cta(tbase, TC::COLS);
-    return;
-  }
-#if EIK_KPF == 2
-  // kernel spectra: component j+1's values are loaded into registers between
-  // the inverse transform of component j and its stores (the stores and the
-  // TMEM reload of X cover the load latency; v and kn are the only live
-  // arrays there), and warmed in L2 one transform ahead of that
-  double kn[LN::EPT];
-  if (valid) {
-    kload_all<TC>(kn, a.ks[0], l, t);
-    if (a.n_comp > 1) kprefetch_all<TC>(a.ks[1], l, t);
-  }
-#pragma unroll 1
-  for (int j = 0; j < a.n_comp; ++j) {
-    tmem_get(ta, v);
-    if (valid) {
-      kapply_all<LN>(v, kn, a.ks[j], t);
-      if (j + 2 < a.n_comp) kprefetch_all<TC>(a.ks[j + 2], l, t);
-    }
-    fft_line<LN, true>(v, t, xb, tws);
-    if (valid && j + 1 < a.n_comp) kload_all<TC>(kn, a.ks[j + 1], l, t);
-#pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) {
-      if (LN::L > 0 && LN::upper_in(r)) continue;
-      const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out) *comp_dst(a, j, item, l, n) = v[r];
-    }
-  }
-  tmem_free_cta(tbase, TC::COLS);
-  return;
-#endif
-#if EIK_KPF
-  if constexpr (TC::TSTORE && OUT == OUT_COMPS) {
-    if (a.tstore) {
-      // outputs through shared memory and TMA: tile slot (n * LPC + line)
-      // (dynamic shared memory base rounded up to 128 bytes as well)
-      char* sbase = reinterpret_cast<char*>(smem);
-      const uint32_t mis = smem_u32(sbase) & 127u;
-      double2* stg = reinterpret_cast<double2*>(sbase + TC::TSTORE_OFF + (mis ? 128u - mis : 0u));
-      if (valid) kprefetch_all<TC>(a.ks[0], l, t);
+    } else {
+      if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
+      else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
+      fft_line<LN, false, HALF>(v, t, xb, tws);
+      tmem_put(ta, v);
+      // kernel spectra: the next component's lines are prefetched into L1 one
+      // transform ahead (no registers held across the FFT); loaded at use
+      if (valid && !EIK_DBG_NOK) kprefetch_all<TC>(a.ks[0], lk, t, bx);
+      next_prefetch();
 #pragma unroll 1
       for (int j = 0; j < a.n_comp; ++j) {
         tmem_get(ta, v);
-        if (valid) {
+        if (valid && !EIK_DBG_NOK) {
           double kn[LN::EPT];
-          kload_all<TC>(kn, a.ks[j], l, t);
-          if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], l, t);
-          kapply_all<LN>(v, kn, a.ks[j], t);
+          kload_all<TC>(kn, a.ks[j], lk, t, bx);
+          if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], lk, t, bx);
+          kapply_all<LN>(v, kn, a.ks[j], t, mir);
         }
         fft_line<LN, true>(v, t, xb, tws);
-        if (j > 0) {  // the previous component's boxes have been read out of the tile
-          if (threadIdx.x == 0) bulk_wait_read0();
-          __syncthreads();
-        }
 #pragma unroll
         for (int r = 0; r < LN::EPT; ++r) {
           if (LN::L > 0 && LN::upper_in(r)) continue;
           const int n = LN::in_idx(t, r);
-          if (n < a.n_out) stg[n * LPC + line] = v[r];
-        }
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          for (int y = 0; y < a.n_out; y += 256)
-            tma_store_3d(&a.umap[j], stg + y * LPC, (int)(blockIdx.x * LPC * 2), y, (int)item);
-          bulk_commit();
+          if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) {
+            double2* dst = comp_dst(a, j, item, l, n);
+            *dst = a.accum ? cadd(*dst, v[r]) : v[r];
+          }
         }
       }
-      if (threadIdx.x == 0) bulk_wait_read0();
-      tmem_free_cta(tbase, TC::COLS);
-      return;
-    }
-  }
-  // kernel spectra: the next component's lines are prefetched into L1 one
-  // transform ahead (no registers held across the FFT); loaded at use
-#ifndef EIK_DBG_NOK
-#define EIK_DBG_NOK 0
-#endif
-#ifndef EIK_DBG_NOST
-#define EIK_DBG_NOST 0
-#endif
-  if (valid && !EIK_DBG_NOK) kprefetch_all<TC>(a.ks[0], l, t);
-#pragma unroll 1
-  for (int j = 0; j < a.n_comp; ++j) {
-    tmem_get(ta, v);
-    if (valid && !EIK_DBG_NOK) {
-      double kn[LN::EPT];
-      kload_all<TC>(kn, a.ks[j], l, t);
-      if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], l, t);
-      kapply_all<LN>(v, kn, a.ks[j], t);
-    }
-#else
-  double kn[LN::EPT];
-  if (valid) {
-    kload_all<TC>(kn, a.ks[0], l, t);
-  }
-#pragma unroll 1
-  for (int j = 0; j < a.n_comp; ++j) {
-    tmem_get(ta, v);
-    if (valid) {
-#pragma unroll
-      for (int r = 0; r < LN::EPT; ++r) v[r] = kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M);
-      if (j + 1 < a.n_comp) {
-        kload_all<TC>(kn, a.ks[j + 1], l, t);
-      }
-    }
-#endif
-    fft_line<LN, true>(v, t, xb, tws);
-#pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) {
-      if (LN::L > 0 && LN::upper_in(r)) continue;
-      const int n = LN::in_idx(t, r);
-      if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) *comp_dst(a, j, item, l, n) = v[r];
     }
   }
   tmem_free_cta(tbase, TC::COLS);
@@ -1205,6 +1090,7 @@ struct RowArgs {
   int64_t split_stride;
   const double2* comp[MAXC];
   int n_comp;
+  int64_t tiles, items;  // persistent row kernel (set by the launcher): tiles of LPC rows per item, items
   int c_phi, c_grad, ngrad, c_hess, c_sign, sign_mode, n_raw;  // component slots (-1 absent)
   double scale, tau, inv_tau;
   double* S;
@@ -1223,13 +1109,17 @@ struct RowArgs {
 };
 
 // Per-line prefetch state of the row pass (RowCfg::FEED): xs holds the row
-// being consumed / in flight; `bar` completes when it has landed.
+// being consumed / in flight; `bar` completes when it has landed.  The fetch
+// sequence runs ahead of the consumption across the tiles of the persistent
+// CTA: (tile, component 0..ncomp-1), (tile + gridDim.x, 0..), ...
 struct RowFeed {
   double2* xs;
   uint64_t* bar;
   uint32_t phase;
-  int next;   // next component to fetch
-  int total;  // components this CTA processes, in order 0..total-1
+  int ftile;  // tile of the next fetch
+  int fcomp;  // component of the next fetch
+  int ncomp;  // components per row, in order 0..ncomp-1
+  int64_t froff;  // spectral-row offset of the line's row in tile ftile (-1: past the last row)
 };
 
 // c2r pre-twist of one half-spectrum row (X[k], k in [0, M]) into the complex
@@ -1266,27 +1156,46 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   extern __shared__ double2 smem[];
   const int line = threadIdx.x / LN::TPL;
   const int t = threadIdx.x % LN::TPL;
-  const int64_t row = a.row0 + (int64_t)blockIdx.x * LPC + line;
-  const bool valid = row < a.row_end;
-  const int64_t item = a.item0 + blockIdx.y;
   using RC = RowCfg<LH>;
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + RC::TWQ;
-  const int64_t rb = valid ? row % a.rows_a : 0;
-  const int64_t roff = item * a.comp_item +
-                       (valid ? (row / a.rows_a) * a.stride_a + (rb >> a.split_shift) * a.split_stride +
-                                    (rb & ((int64_t(1) << a.split_shift) - 1)) * a.stride_b
-                              : 0);
+  // persistent: tiles of LPC rows, tile index fastest, then items (a.tiles per item)
+  const int tiles = (int)a.tiles;
+  const int total = tiles * (int)a.items;
+  // spectral-row offset of this line's row in tile `tl` (false: past the last row)
+  auto row_of = [&](int tl, int64_t& row, int64_t& item) -> bool {
+    const int it = tl / tiles;
+    row = a.row0 + (int64_t)(tl - it * tiles) * LPC + line;
+    item = a.item0 + it;
+    return row < a.row_end;
+  };
+  auto roff_of = [&](int64_t row, int64_t item) -> int64_t {
+    const int64_t rb = row % a.rows_a;
+    return item * a.comp_item + (row / a.rows_a) * a.stride_a + (rb >> a.split_shift) * a.split_stride +
+           (rb & ((int64_t(1) << a.split_shift) - 1)) * a.stride_b;
+  };
   constexpr uint32_t ROW_BYTES = (LN::M + 1) * sizeof(double2);
-  RowFeed fd{nullptr, nullptr, 0u, 0, a.n_raw > 0 ? a.n_raw : a.n_comp};
-  auto feed_issue = [&]() {  // thread 0 of the line: start fetching component fd.next
-    if (RC::FEED && t == 0 && valid && fd.next < fd.total) {
-      fence_proxy_async_smem();
-      mbar_expect_tx(fd.bar, ROW_BYTES);
-      bulk_g2s(fd.xs, a.comp[fd.next] + roff, ROW_BYTES, fd.bar);
+  RowFeed fd{nullptr, nullptr, 0u, (int)blockIdx.x, 0, a.n_raw > 0 ? a.n_raw : a.n_comp, -1};
+  auto feed_tile = [&]() {  // offset of the fetch tile's row (once per tile: 64-bit divisions)
+    int64_t frow, fitem;
+    fd.froff = (fd.ftile < total && row_of(fd.ftile, frow, fitem)) ? roff_of(frow, fitem) : -1;
+  };
+  auto feed_issue = [&]() {  // thread 0 of the line: start the next fetch of the sequence
+    if constexpr (RC::FEED) {
+      if (fd.ftile < total) {
+        if (t == 0 && fd.froff >= 0) {
+          fence_proxy_async_smem();
+          mbar_expect_tx(fd.bar, ROW_BYTES);
+          bulk_g2s(fd.xs, a.comp[fd.fcomp] + fd.froff, ROW_BYTES, fd.bar);
+        }
+        if (++fd.fcomp == fd.ncomp) {
+          fd.fcomp = 0;
+          fd.ftile += gridDim.x;
+          if (t == 0) feed_tile();
+        }
+      }
     }
-    ++fd.next;
   };
   if constexpr (RC::FEED) {
     char* fb = reinterpret_cast<char*>(smem) + ((RC::BASE_BYTES + 15) & ~size_t(15));
@@ -1297,27 +1206,27 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
+    if (t == 0) feed_tile();
     feed_issue();
-#if EIK_L2PF
-    // first component's row of the CTA one resident wave later
-    int64_t bx, by;
-    if (t == 0 && a.comp_item > 0 && cta_ahead(148 * RC::MINB, bx, by)) {
-      const int64_t r2 = a.row0 + bx * LPC + line;
-      if (r2 < a.row_end) {
-        const int64_t rb2 = r2 % a.rows_a;
-        const int64_t off2 = (a.item0 + by) * a.comp_item + (r2 / a.rows_a) * a.stride_a +
-                             (rb2 >> a.split_shift) * a.split_stride +
-                             (rb2 & ((int64_t(1) << a.split_shift) - 1)) * a.stride_b;
-        bulk_prefetch_l2(a.comp[0] + off2, ROW_BYTES);
-      }
-    }
-#endif
   }
+  twq_fill(twq, LH + 1, a.tw, a.lmax);
+  st_fill<LN>(sts, a.tw, a.lmax);
+  __syncthreads();
+  const bool even = (a.n_out & 1) == 0;
+  unsigned cnt = 0;
+
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+  int64_t row, item;
+  const bool valid = row_of(tile, row, item);
+  const int64_t roff = valid ? roff_of(row, item) : item * a.comp_item;
   // the current component's row: from the prefetch buffer (waits for it) or global
   auto row_src = [&]() -> const double2* {
     if constexpr (RC::FEED) {
-      if (valid) mbar_wait(fd.bar, fd.phase);
-      fd.phase ^= 1u;
+      if (valid) {
+        mbar_wait(fd.bar, fd.phase);
+        fd.phase ^= 1u;
+      }
       return fd.xs;
     } else {
       return nullptr;
@@ -1330,11 +1239,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
       feed_issue();
     }
   };
-  twq_fill(twq, LH + 1, a.tw, a.lmax);
-  st_fill<LN>(sts, a.tw, a.lmax);
-  __syncthreads();
   const int64_t obase = item * a.N + row * a.n_out;
-  const bool even = (a.n_out & 1) == 0;
 
   auto put = [&](double* dst, int r, double x0, double x1) {
     const int n = 2 * LN::in_idx(t, r);
@@ -1367,7 +1272,6 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
     feed_next();
     fft_line<LN, true>(z, t, xb, TwSrc{sts, twq, LN::L + 1, 0u});
   };
-  unsigned cnt = 0;
   if (a.c_phi >= 0) {
     row_c2r(a.comp[a.c_phi] + roff);
 #pragma unroll
@@ -1465,6 +1369,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
       put(a.raw[j], r, x0, x1);
     }
   }
+  }  // tiles
   if (a.uf_count) {
     const unsigned tot = __reduce_add_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.uf_count, (unsigned long long)tot);

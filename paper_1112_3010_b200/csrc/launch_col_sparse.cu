@@ -13,15 +13,7 @@ static bool use_tmem() {
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
-  using C = TmCfg<L, tm_lpcx(L, OUT)>;
-  auto k = col_tmem_kernel<L, IN, OUT, HALF>;
-  CK(prep_kernel_attr(k, C::SMEM_BYTES));
-  const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
-  if (tiles <= 0 || items <= 0) return EIK_OK;
-  if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
-  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);
-  CK(cudaGetLastError());
-  return EIK_OK;
+  return launch_tmem_persistent<L, IN, OUT, HALF>(a, items, st);
 }
 
 template <int L, int IN, int OUT, bool HALF>

@@ -6,9 +6,21 @@ int launch_row_t(const RowArgs& a, int64_t items, cudaStream_t st) {
   auto k = a.c_hess >= 0 ? row_kernel<LH, true> : row_kernel<LH, false>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
   const int64_t tiles = (a.row_end - a.row0 + C::LPC - 1) / C::LPC;
-  if (tiles <= 0) return EIK_OK;
-  if (items > 65535) return fail(EIK_EVALIDATION, "too many items in one launch");
-  k<<<dim3((unsigned)tiles, (unsigned)items), C::NT, C::SMEM_BYTES, st>>>(a);
+  if (tiles <= 0 || items <= 0) return EIK_OK;
+  // persistent: one resident wave of CTAs walks the (item, tile) list, the row
+  // feed running one component ahead across tiles (EIK_PERSIST=0: one CTA per tile)
+  const int pm = persist_mode();
+  const bool persist = pm < 0 ? true : pm > 0;
+  RowArgs b = a;
+  b.tiles = tiles;
+  b.items = items;
+  const int64_t total = tiles * items;
+  if (total > 0x7fffffffLL) return fail(EIK_EVALIDATION, "too many row tiles in one launch");
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::NT, C::SMEM_BYTES));
+  const int64_t wave = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+  const int64_t grid = persist ? (total < wave ? total : wave) : total;
+  k<<<(unsigned)grid, C::NT, C::SMEM_BYTES, st>>>(b);
   CK(cudaGetLastError());
   return EIK_OK;
 }

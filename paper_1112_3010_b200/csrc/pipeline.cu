@@ -112,6 +112,7 @@ struct KDev {
   int ktype = 0;
   int imag = 0;
   int odd0 = 0;
+  int odd1 = 0;  // 3-D: odd along axis 1 (k1-mirrored lines change sign)
   double sign = 1.0;
   DevBuf buf;  // folded real/imag spectrum [(M0/2+1) x lines]
   DevBuf kp;   // register-order copy for the 2-D column kernels (KSpec::perm), or empty
@@ -125,6 +126,10 @@ struct eik_plan {
   int c[3] = {1, 1, 1}, M[3] = {1, 1, 1}, L[3] = {0, 0, 0};
   int64_t N = 0, H = 0, lines = 0;
   int64_t ks_l0 = 0, ks_lines = 0;  // spectral lines [ks_l0, ks_l0 + ks_lines) whose kernel spectra are stored
+  // 3-D: the spectra are stored folded along axis 1 (every kernel is even or odd
+  // there): the plan covers k1 in [k1_begin, k1_begin + k1_count) and stores the
+  // lines of the folded indices min(k1, M1 - k1) in [fold_f0, fold_f0 + ks_lines / H)
+  int64_t k1_begin = 0, k1_count = 0, fold_f0 = 0;
   double h = 1.0, tau = 1.0;
   uint32_t fields = 0;
   int device = 0;
@@ -314,11 +319,12 @@ int spectrum_of(eik_plan* p, const GenArgs& g, int part, double* dst_re, double2
 }
 
 int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, int n_odd_axes, bool odd0,
-               double sign, double2* work, cudaStream_t st, double tau = 0.0) {
+               double sign, double2* work, cudaStream_t st, double tau = 0.0, bool odd1 = false) {
   auto k = std::make_unique<KDev>();
   k->ktype = ktype;
   k->imag = n_odd_axes % 2;
   k->odd0 = odd0 ? 1 : 0;
+  k->odd1 = (p->D == 3 && odd1) ? 1 : 0;
   k->sign = sign;
   const int64_t n = (int64_t)(p->M[0] / 2 + 1) * p->ks_lines;
   CK(k->buf.ensure(n * sizeof(double)));
@@ -351,6 +357,7 @@ KSpec kspec_of(const eik_plan* p, const KDev& k) {
   s.ld = p->ks_lines;
   s.imag = k.imag;
   s.odd0 = k.odd0;
+  s.odd1 = k.odd1;
   if (k.kp.bytes) {
     s.perm = k.kp.as<double>();
     s.odd0 = k.kp_folded ? k.odd0 : 0;
@@ -432,8 +439,18 @@ int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double 
     if (p->D != 3) return fail(EIK_EVALIDATION, "k1 slabs apply to 3-D plans");
     if (k1_begin < 0 || k1_count < 1 || k1_begin + k1_count > p->M[1])
       return fail(EIK_EVALIDATION, "k1 slab outside the padded axis");
-    p->ks_l0 = k1_begin * p->H;
-    p->ks_lines = k1_count * p->H;
+  }
+  if (p->D == 3) {
+    // folded storage along axis 1: the image of the slab under k1 -> min(k1, M1 - k1) is an interval
+    p->k1_begin = k1_count >= 0 ? k1_begin : 0;
+    p->k1_count = k1_count >= 0 ? k1_count : p->M[1];
+    const int64_t M1 = p->M[1], half = M1 / 2, a = p->k1_begin, b = p->k1_begin + p->k1_count - 1;
+    auto fold = [&](int64_t k) { return k > half ? M1 - k : k; };
+    int64_t lo = std::min(fold(a), fold(b)), hi = std::max(fold(a), fold(b));
+    if (a <= half && half <= b) hi = half;
+    p->fold_f0 = lo;
+    p->ks_l0 = lo * p->H;
+    p->ks_lines = (hi - lo + 1) * p->H;
   }
   cudaStream_t st = nullptr;
   const bool need_phi = fields & (EIK_FIELD_PHI | EIK_FIELD_S | EIK_FIELD_GRAD | EIK_FIELD_HESS);
@@ -449,7 +466,9 @@ int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double 
       p->k_grad = (int)p->kdist.size();
       for (int a = 0; a < dim; ++a) {
         const int internal_axis = a + p->ref0;
-        if ((rc = add_kernel(p.get(), p->kdist, KT_GRAD0 + a, 1, internal_axis == 0, 1.0, work, st))) return rc;
+        if ((rc = add_kernel(p.get(), p->kdist, KT_GRAD0 + a, 1, internal_axis == 0, 1.0, work, st, 0.0,
+                             internal_axis == 1)))
+          return rc;
       }
     }
     if (fields & EIK_FIELD_HESS) {
@@ -465,7 +484,7 @@ int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double 
     }
     if (fields & EIK_FIELD_DEGREE) {
       for (int a = 0; a < 3; ++a)
-        if ((rc = add_kernel(p.get(), p->ksign, KT_RAT3_0 + a, 1, a == 0, 1.0, work, st))) return rc;
+        if ((rc = add_kernel(p.get(), p->ksign, KT_RAT3_0 + a, 1, a == 0, 1.0, work, st, 0.0, a == 1))) return rc;
     }
     CK(cudaDeviceSynchronize());
     p->work.release();
@@ -521,9 +540,16 @@ struct Roles {
 
 int set_components(const eik_plan* p, bool sign_group, const Roles& r, ColArgs& x, double2* const* W,
                    int64_t k1_offset_lines) {
+  if (p->D == 3) {  // folded storage along axis 1: the kernels map pass lines to stored lines
+    x.fold_H = (int)p->H;
+    x.fold_M1 = p->M[1];
+    x.fold_k1base = k1_offset_lines / p->H;
+    x.fold_f0 = p->fold_f0;
+  }
   auto ks = [&](const KDev& k) {
     KSpec s = kspec_of(p, k);
-    s.re += k1_offset_lines - p->ks_l0;  // k1-slab: lines [k1b*H, ...) of the global layout
+    if (p->D == 3) return s;
+    s.re += k1_offset_lines - p->ks_l0;
     if (k1_offset_lines != p->ks_l0) {  // the register-order copy covers the plan's own lines only
       s.perm = nullptr;
       s.odd0 = k.odd0;
@@ -718,7 +744,7 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
 int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks, int64_t B, const Roles& r,
                double2* const* W, cudaStream_t st, const PeerBlk* pb = nullptr) {
   const int64_t H = p->H;
-  if (k1b * H < p->ks_l0 || (k1b + ks) * H > p->ks_l0 + p->ks_lines)
+  if (k1b < p->k1_begin || k1b + ks > p->k1_begin + p->k1_count)
     return fail(EIK_EVALIDATION, "k1 slab not covered by the plan's kernel spectra");
   ColArgs a = col_defaults(p);
   a.nlines = ks * H;
@@ -750,9 +776,10 @@ using ChunkFn = std::function<int(int64_t, int64_t, int64_t, int64_t)>;
 
 int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, int64_t ks, int64_t B,
                 RowArgs ra, cudaStream_t st, const std::function<int(int, bool)>& mark,
-                const ChunkFn& on_chunk = nullptr) {
+                const ChunkFn& on_chunk = nullptr, double* raw_dest = nullptr) {
   const int64_t H = p->H;
-  const int nc = r.n_comp();
+  // raw_dest: one component, written as the scaled real-space convolution (no epilogue)
+  const int nc = raw_dest ? 1 : r.n_comp();
   int rc;
   if (p->D == 3) {
     LinesArgs la = lines_defaults(p);
@@ -796,6 +823,13 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
   ra.ngrad = r.ngrad;
   ra.c_hess = r.hess ? 1 + r.ngrad : -1;
   ra.c_sign = r.sign ? r.n_dist() : -1;
+  if (raw_dest) {
+    ra.c_phi = ra.c_grad = ra.c_hess = ra.c_sign = -1;
+    ra.ngrad = 0;
+    ra.n_raw = 1;
+    ra.raw[0] = raw_dest;
+    ra.raw_tau[0] = 0.0;
+  }
   ra.sign_mode = p->dim == 2 ? 1 : 2;
   double scale = 1.0;
   for (int a = 0; a < p->D; ++a) scale /= (double)p->M[a];
@@ -836,6 +870,118 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
     }
   }
   return mark(EIK_PASS_ROW, true);
+}
+
+
+// ---------------------------------------------------------------------------
+// Streamed 3-D schedule (one GPU, grids whose fused buffers exceed the device:
+// C4 at 1024^3).  One spectrum slot V and one component slot W are live at a
+// time: each distance component runs its own axis-0 pass (the forward transform
+// of V is repeated per component), is brought back to real space unscaled by
+// the row kernel's raw mode, and a last elementwise pass applies the epilogue
+// (the same double operations as the fused row epilogue).  The sign group
+// accumulates W += IFFT0(K_i FFT0(V_i)) over its three flux inputs.  The
+// impulse DFT's T is written inside V (first c1 entries of every axis-1 line)
+// and transformed in place.
+
+// impulse DFT along axis 2 + in-place FFT along axis 1 of ONE input -> V[i0][k1][k2]
+int pass_planes_inplace(eik_plan* p, bool sg, const int64_t* nodes, int64_t K, const double* w, double2* V,
+                        cudaStream_t st) {
+  const int64_t H = p->H, c0 = p->c[0], c1 = p->c[1], c2 = p->c[2], M1 = p->M[1];
+  if (H > (int64_t)ROWDFT_NF * ROWDFT_NT) return fail(EIK_EVALIDATION, "last axis too long for the row DFT");
+  if (c0 > 65535) return fail(EIK_EVALIDATION, "axis 0 too long for the streamed planes pass");
+  DevBuf& rid = sg ? p->srowid : p->rowid;
+  DevBuf& cl = sg ? p->scols : p->cols;
+  DevBuf& rp = sg ? p->srowptr : p->rowptr;
+  int rc = prep_nodes(p, nodes, nullptr, K, 1, c0 * c1 * c2, c0 * c1, c2, rid, cl, rp, st);
+  if (rc) return rc;
+  RowDftArgs ra{};
+  ra.rowptr = rp.as<int64_t>();
+  ra.cols = cl.as<int32_t>();
+  ra.n_in = 1;
+  ra.w[0] = w;
+  ra.out[0] = V;
+  ra.rows_per_item = c1;  // "items" are the planes i0: row (i0, i1) lands at V[i0][i1][.]
+  ra.H = H;
+  ra.out_item = M1 * H;
+  ra.last_shift = p->lmax - p->L[2];
+  ra.last_mask = p->M[2] - 1;
+  ra.tw = p->tw.as<double2>();
+  CK(launch_impulse_rows(ra, 1, c1, c0, st));
+  LinesArgs la = lines_defaults(p);
+  la.in[0] = V;
+  la.out[0] = V;
+  la.nlines = c0 * H;
+  la.inner = H;
+  la.outer_in = la.outer_out = M1 * H;
+  la.es_in = la.es_out = H;
+  la.n_valid = (int)c1;
+  la.n_out = (int)M1;
+  return launch_lines<false, true>(p->L[1], la, 1, st);
+}
+
+// axis-0 pass of one kernel: W (+)= IFFT0(K FFT0(V)), rows [0, c0)
+int pass_axis0_single(eik_plan* p, const double2* V, const KDev& k, double2* W, bool accum, cudaStream_t st) {
+  const int64_t H = p->H, M1 = p->M[1];
+  ColArgs a = col_defaults(p);
+  a.nlines = M1 * H;
+  a.n_valid = p->c[0];
+  a.n_out = p->c[0];
+  a.n_in = 1;
+  a.din[0] = V;
+  a.din_es = M1 * H;
+  a.din_item = (int64_t)p->c[0] * M1 * H;
+  a.out_es = M1 * H;
+  a.out_item = (int64_t)p->c[0] * M1 * H;
+  a.fold_H = (int)H;
+  a.fold_M1 = (int)M1;
+  a.fold_k1base = 0;
+  a.fold_f0 = p->fold_f0;
+  a.ks[0] = kspec_of(p, k);
+  a.out[0] = W;
+  a.n_comp = 1;
+  a.accum = accum ? 1 : 0;
+  return launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, 1, st);
+}
+
+struct StreamEpi {
+  int64_t N;
+  double* phi_raw;   // scaled phi (may alias S or phi_out)
+  double* S;
+  double* phi_out;
+  uint8_t* uf;
+  unsigned long long* uf_count;
+  double* grad[3];   // in: scaled numerators, out: ratios (in place)
+  double* mu_raw;    // scaled sign convolution (may alias mu)
+  double* mu;
+  uint8_t* mask;
+  double tau;
+};
+
+// Elementwise epilogue of the streamed schedule: the operations of row_kernel's
+// fused epilogue (3-D: no Hessian, ratios by division) on the raw fields.
+__global__ void stream_epilogue_kernel(const StreamEpi e) {
+  unsigned cnt = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e.N; i += (int64_t)gridDim.x * blockDim.x) {
+    if (e.phi_raw) {
+      const double phi = e.phi_raw[i];
+      cnt += (phi <= 0.0);
+      for (int d = 0; d < 3; ++d)
+        if (e.grad[d]) e.grad[d][i] = e.grad[d][i] / phi;
+      if (e.phi_out && e.phi_out != e.phi_raw) e.phi_out[i] = phi;
+      if (e.uf) e.uf[i] = phi <= 0.0;
+      if (e.S) e.S[i] = phi > 0.0 ? (-e.tau) * log(phi) : __longlong_as_double(0x7ff8000000000000LL);
+    }
+    if (e.mu_raw) {
+      const double m = -e.mu_raw[i] / 12.566370614359172;
+      if (e.mu) e.mu[i] = m;
+      if (e.mask) e.mask[i] = rint(m) >= 1.0;
+    }
+  }
+  if (e.uf_count) {
+    const unsigned tot = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(e.uf_count, (unsigned long long)tot);
+  }
 }
 
 }  // namespace
@@ -1041,9 +1187,31 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
   const bool waves = p->D == 2 && want_phi && !want_sign && wave_env > 0 && B > wave_env && rowdft_on == 1 &&
                      p->H <= (int64_t)ROWDFT_NF * ROWDFT_NT;
   const int64_t BW = waves ? wave_env : B;
-  CK(p->comp.ensure((size_t)n_comp * BW * ce * sizeof(double2)));
+  // 3-D, one item: the streamed schedule (one V and one W slot, see
+  // pass_planes_inplace) when the fused buffers do not fit the device;
+  // EIK_STREAM3D=1 forces it, =0 forbids it
+  bool streamed = false;
+  if (p->D == 3 && B == 1 && !(flags & EIK_SLAB_P2P)) {
+    const char* e = std::getenv("EIK_STREAM3D");
+    if (e && (e[0] == '0' || e[0] == '1')) {
+      streamed = e[0] == '1';
+    } else {
+      const int n_in_max = std::max(want_phi ? 1 : 0, want_sign ? 3 : 0);
+      const size_t need = (size_t)(n_in_max + n_comp) * ce * sizeof(double2) +
+                          (size_t)n_in_max * p->c[0] * p->c[1] * p->H * sizeof(double2);
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      const size_t avail = fr + p->vin.bytes + p->comp.bytes + p->trows.bytes;
+      streamed = need + (size_t(1) << 30) > avail;
+    }
+  }
+  if (streamed) {
+    p->trows.release();
+    CK(p->vin.ensure((size_t)ce * sizeof(double2)));
+  }
+  CK(p->comp.ensure((size_t)(streamed ? 1 : n_comp * BW) * ce * sizeof(double2)));
   std::vector<double2*> W(n_comp);
-  for (int j = 0; j < n_comp; ++j) W[j] = p->comp.as<double2>() + (int64_t)j * BW * ce;
+  for (int j = 0; j < n_comp; ++j) W[j] = p->comp.as<double2>() + (streamed ? 0 : (int64_t)j * BW * ce);
   int rc;
   if (waves) {
     // node CSR over the whole batch once; the waves index into it
@@ -1090,7 +1258,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     if ((rc = sign_first ? sign_group() : dist_group())) return rc;
     if ((rc = sign_first ? dist_group() : sign_group())) return rc;
     if (fork) CK(cudaStreamWaitEvent(st, p->ev_join, 0));
-  } else {
+  } else if (!streamed) {
     const int n_in_max = std::max(want_phi ? 1 : 0, want_sign ? 3 : 0);
     CK(p->vin.ensure((size_t)n_in_max * B * ce * sizeof(double2)));
     double2* V[3];
@@ -1132,8 +1300,61 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     CK(cudaStreamWaitEvent(st, p->ev_copies, 0));
     p->copies_pending = false;
   }
+  // streamed 3-D schedule: every component through the one V / W pair, then the elementwise epilogue
+  auto run_streamed = [&]() -> int {
+    int rc2;
+    double2* V1 = p->vin.as<double2>();
+    double2* W1 = p->comp.as<double2>();
+    std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
+    // scratch for raw fields whose output was not requested
+    const bool need_phi_scratch = want_phi && !o_S && !o_phi;
+    const bool need_mu_scratch = want_sign && !o_mu;
+    if (need_phi_scratch || need_mu_scratch) CK(p->work.ensure((size_t)2 * p->N * sizeof(double)));
+    StreamEpi e{};
+    e.N = p->N;
+    e.tau = p->tau;
+    RowArgs rr = ra;  // scale etc. are filled by pass_finish; outputs unused in raw mode
+    rr.S = nullptr; rr.mu = nullptr; rr.mask = nullptr; rr.uf = nullptr; rr.phi_out = nullptr; rr.uf_count = nullptr;
+    for (int d = 0; d < 3; ++d) rr.grad[d] = rr.hess[d] = nullptr;
+    if (want_phi) {
+      if ((rc2 = mark(EIK_PASS_COL, false))) return rc2;
+      if ((rc2 = pass_planes_inplace(p, false, d_nodes, in->n_nodes, nullptr, V1, st))) return rc2;
+      e.phi_raw = o_S ? o_S : (o_phi ? o_phi : p->work.as<double>());
+      if ((rc2 = pass_axis0_single(p, V1, *p->kdist[p->k_exp], W1, false, st))) return rc2;
+      if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, e.phi_raw))) return rc2;
+      for (int d = 0; d < r.ngrad; ++d) {
+        if (!o_g[d]) continue;
+        if ((rc2 = pass_axis0_single(p, V1, *p->kdist[p->k_grad + d], W1, false, st))) return rc2;
+        if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, o_g[d]))) return rc2;
+        e.grad[d] = o_g[d];
+      }
+      e.S = o_S;
+      e.phi_out = o_phi;
+      e.uf = o_uf;
+      e.uf_count = ra.uf_count;
+      if ((rc2 = mark(EIK_PASS_COL, true))) return rc2;
+    }
+    if (want_sign) {
+      if ((rc2 = mark(EIK_PASS_COL_SIGN, false))) return rc2;
+      if (want_fill && (rc2 = eik_fill_bits(d_snodes, Ks, p->N, fbits, st))) return rc2;
+      for (int i = 0; i < 3; ++i) {
+        if ((rc2 = pass_planes_inplace(p, true, d_snodes, Ks, d_sw + (int64_t)i * Ks, V1, st))) return rc2;
+        if ((rc2 = pass_axis0_single(p, V1, *p->ksign[i], W1, i > 0, st))) return rc2;
+      }
+      e.mu_raw = o_mu ? o_mu : p->work.as<double>() + p->N;
+      if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, e.mu_raw))) return rc2;
+      e.mu = o_mu;
+      e.mask = o_mask;
+      if ((rc2 = mark(EIK_PASS_COL_SIGN, true))) return rc2;
+    }
+    if ((rc2 = mark(EIK_PASS_ROW, false))) return rc2;
+    stream_epilogue_kernel<<<148 * 8, 256, 0, st>>>(e);
+    CK(cudaGetLastError());
+    return mark(EIK_PASS_ROW, true);
+  };
   // the row pass (and, in wave mode, each wave's column pass + row pass)
   auto finish = [&](const ChunkFn& on_chunk) -> int {
+    if (streamed) return run_streamed();
     if (!waves) return pass_finish(p, W.data(), r, p->c[0], p->M[1], B, ra, st, mark, on_chunk);
     std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
     int rc2;
@@ -1158,7 +1379,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     }
     return mark(EIK_PASS_COL, true);
   };
-  if (host_out && !slots.empty() && !prof && NB >= (int64_t(1) << 22)) {
+  if (host_out && !slots.empty() && !prof && !streamed && NB >= (int64_t(1) << 22)) {
     // D2H of each finished chunk of rows on a copy stream, overlapping the rest
     // of the row pass (the end-to-end path is PCIe-bound on the outputs)
     // two copy streams: consecutive copies alternate between copy engines

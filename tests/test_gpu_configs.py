@@ -153,6 +153,32 @@ def test_c4_scaled_eik_run_vs_oracle(c4_128):
     assert 0.15 < inside < 0.25  # sphere of radius 43.75 in a 128^3 box: 0.17
 
 
+def test_c4_scaled_streamed_vs_oracle_and_fused(c4_128, monkeypatch):
+    """The streamed one-GPU schedule (one V and one W slot; what C4 at 1024^3 runs
+    on a single B200): against the oracle, and S / grad bit-identical to the fused
+    schedule (same arithmetic per node; mu sums its three inputs after the
+    inverse transforms instead of before, so it agrees to rounding)."""
+    from paper_1112_3010_b200 import engine
+
+    d, ref = c4_128
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("EIK_STREAM3D", mode)
+        dt = engine.DistanceTransform(d["grid"], 0.75, grad=True, sign=True)
+        outs[mode] = dt.run_host(d["nodes"], sign_nodes=d["sign_nodes"], sign_weights=d["sign_weights"])
+    _check_c4(outs["1"], ref, d["sign_nodes"], "streamed")
+    assert np.array_equal(outs["0"]["S"], outs["1"]["S"], equal_nan=True)
+    for a in range(3):
+        assert np.array_equal(outs["0"]["grad"][a], outs["1"]["grad"][a], equal_nan=True)
+    assert np.abs(outs["0"]["mu"] - outs["1"]["mu"]).max() <= T3_ATOL
+    assert np.array_equal(outs["0"]["mask"], outs["1"]["mask"])
+    # distance-only plan through the streamed schedule
+    monkeypatch.setenv("EIK_STREAM3D", "1")
+    dt = engine.DistanceTransform(d["grid"], 0.75, grad=True, sign=False)
+    o2 = dt.run_host(d["nodes"])
+    assert np.array_equal(o2["S"], outs["0"]["S"], equal_nan=True)
+
+
 @pytest.mark.parametrize("world,p2p", [(2, False), (2, True), (4, True)])
 def test_c4_scaled_slab_vs_oracle(c4_128, world, p2p):
     import torch
