@@ -119,7 +119,14 @@ int eik_plan_info(const eik_plan* plan, int64_t* padded, int64_t* lines, int64_t
 
 /* One pass of the hot path over a batch: phi, S, gradient, Hessian from one
  * shared transform of delta_Y plus the sign field (R/distance.py:114-122,
- * R/derivatives.py:64-112, R/sign.py:108-163). */
+ * R/derivatives.py:64-112, R/sign.py:108-163).
+ * 3-D plans keep their kernel spectra folded along all three axes (every
+ * kernel is even or odd per axis).  A 3-D run of one item whose fused buffers
+ * (one spectrum per input, one per component) would not fit the device runs
+ * the streamed schedule instead: one spectrum slot and one component slot,
+ * one axis-0 pass per component, the epilogue applied elementwise at the end
+ * (same arithmetic per node; C4 at 1024^3 on one 180 GB GPU).  EIK_STREAM3D=1/0
+ * in the environment forces / forbids it. */
 int eik_run(eik_plan* plan, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream);
 
 /* Engine-level linear convolution of n_kernels centred kernels (each of shape
@@ -217,7 +224,9 @@ int eik_dd_run(eik_dd_plan* plan, const int64_t* nodes, int64_t n_nodes, const e
 /* tau sweep (the kernel-reuse of R/experiments.py:74-109):
  * one plan caches exp(-|x|/tau_i) spectra for n_taus values; eik_run_sweep
  * transforms delta_Y once and writes S_i = -tau_i log phi_i for every tau
- * (NaN where phi_i <= 0; n_underflow counts those over all taus).  1-D / 2-D. */
+ * (NaN where phi_i <= 0; n_underflow counts those over all taus).  1-D, 2-D
+ * and 3-D grids (3-D: the planes pass is shared, the axis-0 pass runs in
+ * chunks of four tau values). */
 int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const double* taus, int n_taus,
                           int device, eik_plan** out);
 int eik_run_sweep(eik_plan* plan, const int64_t* nodes, int64_t n_nodes, double* const* S, int64_t* n_underflow,

@@ -335,6 +335,29 @@ def degree_from_weights(nodes, weights, spacing, counts):
     return -mu.reshape(-1) / (4.0 * math.pi)
 
 
+def degree_direct_nodes(nodes, weights, query, spacing, counts, chunk=16):
+    """The degree convolution of degree_from_weights (R/sign.py:135-163) as the
+    plain sums it equals, at selected query nodes (flat indices):
+    mu(x) = -(1 / 4 pi) sum_v sum_a w_a(v) o_a / |o|^3, o = h (i_x - i_v), with
+    the zero offset contributing nothing (R/sign.py:97-105).  O(Q K): the exact
+    checker where the FFT oracle does not fit (C4 at 1024^3)."""
+    nodes = np.asarray(nodes, dtype=np.int64)
+    query = np.asarray(query, dtype=np.int64)
+    ijk_v = np.stack(np.unravel_index(nodes, counts), axis=1).astype(np.float64)
+    ijk_q = np.stack(np.unravel_index(query, counts), axis=1).astype(np.float64)
+    w = np.asarray(weights, dtype=np.float64)  # (3, K)
+    out = np.empty(query.size)
+    for lo in range(0, query.size, chunk):
+        o = spacing * (ijk_q[lo:lo + chunk, None, :] - ijk_v[None, :, :])  # (q, K, 3)
+        r2 = np.einsum("qka,qka->qk", o, o)
+        r3 = r2 * np.sqrt(r2)
+        num = np.einsum("qka,ak->qk", o, w)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t = np.where(r2 > 0.0, num / r3, 0.0)
+        out[lo:lo + chunk] = -t.sum(axis=1) / (4.0 * math.pi)
+    return out
+
+
 def direct_local(src, query, tau, hessian=False, cutoff=30.0):
     """s_direct / direct_ratios (R/distance.py:133-152, R/derivatives.py:186-207)
     at selected query points, summing only the sources within dmin + cutoff of

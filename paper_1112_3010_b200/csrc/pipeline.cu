@@ -318,6 +318,20 @@ int spectrum_of(eik_plan* p, const GenArgs& g, int part, double* dst_re, double2
   return launch_col<IN_DENSE, OUT_SPECTRUM, false>(p->L[0], a, 1, st);
 }
 
+// 3-D plans store their kernel spectra folded along axis 1: the image of the
+// k1 slab under k1 -> min(k1, M1 - k1) is an interval of stored lines
+void init_fold(eik_plan* p, int64_t k1_begin, int64_t k1_count) {
+  p->k1_begin = k1_begin;
+  p->k1_count = k1_count;
+  const int64_t M1 = p->M[1], half = M1 / 2, a = k1_begin, b = k1_begin + k1_count - 1;
+  auto fold = [&](int64_t k) { return k > half ? M1 - k : k; };
+  int64_t lo = std::min(fold(a), fold(b)), hi = std::max(fold(a), fold(b));
+  if (a <= half && half <= b) hi = half;
+  p->fold_f0 = lo;
+  p->ks_l0 = lo * p->H;
+  p->ks_lines = (hi - lo + 1) * p->H;
+}
+
 int add_kernel(eik_plan* p, std::vector<std::unique_ptr<KDev>>& v, int ktype, int n_odd_axes, bool odd0,
                double sign, double2* work, cudaStream_t st, double tau = 0.0, bool odd1 = false) {
   auto k = std::make_unique<KDev>();
@@ -440,18 +454,7 @@ int eik_plan_create_slab(int dim, const int64_t* counts, double spacing, double 
     if (k1_begin < 0 || k1_count < 1 || k1_begin + k1_count > p->M[1])
       return fail(EIK_EVALIDATION, "k1 slab outside the padded axis");
   }
-  if (p->D == 3) {
-    // folded storage along axis 1: the image of the slab under k1 -> min(k1, M1 - k1) is an interval
-    p->k1_begin = k1_count >= 0 ? k1_begin : 0;
-    p->k1_count = k1_count >= 0 ? k1_count : p->M[1];
-    const int64_t M1 = p->M[1], half = M1 / 2, a = p->k1_begin, b = p->k1_begin + p->k1_count - 1;
-    auto fold = [&](int64_t k) { return k > half ? M1 - k : k; };
-    int64_t lo = std::min(fold(a), fold(b)), hi = std::max(fold(a), fold(b));
-    if (a <= half && half <= b) hi = half;
-    p->fold_f0 = lo;
-    p->ks_l0 = lo * p->H;
-    p->ks_lines = (hi - lo + 1) * p->H;
-  }
+  if (p->D == 3) init_fold(p.get(), k1_count >= 0 ? k1_begin : 0, k1_count >= 0 ? k1_count : p->M[1]);
   cudaStream_t st = nullptr;
   const bool need_phi = fields & (EIK_FIELD_PHI | EIK_FIELD_S | EIK_FIELD_GRAD | EIK_FIELD_HESS);
   const bool need_sign = fields & (EIK_FIELD_WINDING | EIK_FIELD_DEGREE);
@@ -773,13 +776,18 @@ int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks,
 // chunks and is called after each chunk is queued (host copies overlap the
 // remaining chunks).
 using ChunkFn = std::function<int(int64_t, int64_t, int64_t, int64_t)>;
+struct RawOut {
+  int n = 0;
+  double* dest[MAXC] = {};
+  double tau[MAXC] = {};
+};
 
 int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, int64_t ks, int64_t B,
                 RowArgs ra, cudaStream_t st, const std::function<int(int, bool)>& mark,
-                const ChunkFn& on_chunk = nullptr, double* raw_dest = nullptr) {
+                const ChunkFn& on_chunk = nullptr, const RawOut* raw = nullptr) {
   const int64_t H = p->H;
-  // raw_dest: one component, written as the scaled real-space convolution (no epilogue)
-  const int nc = raw_dest ? 1 : r.n_comp();
+  // raw: W[0..n) are written as scaled real-space convolutions (tau > 0: -tau log), no epilogue
+  const int nc = raw ? raw->n : r.n_comp();
   int rc;
   if (p->D == 3) {
     LinesArgs la = lines_defaults(p);
@@ -823,12 +831,14 @@ int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, i
   ra.ngrad = r.ngrad;
   ra.c_hess = r.hess ? 1 + r.ngrad : -1;
   ra.c_sign = r.sign ? r.n_dist() : -1;
-  if (raw_dest) {
+  if (raw) {
     ra.c_phi = ra.c_grad = ra.c_hess = ra.c_sign = -1;
     ra.ngrad = 0;
-    ra.n_raw = 1;
-    ra.raw[0] = raw_dest;
-    ra.raw_tau[0] = 0.0;
+    ra.n_raw = raw->n;
+    for (int j = 0; j < raw->n; ++j) {
+      ra.raw[j] = raw->dest[j];
+      ra.raw_tau[j] = raw->tau[j];
+    }
   }
   ra.sign_mode = p->dim == 2 ? 1 : 2;
   double scale = 1.0;
@@ -920,8 +930,9 @@ int pass_planes_inplace(eik_plan* p, bool sg, const int64_t* nodes, int64_t K, c
   return launch_lines<false, true>(p->L[1], la, 1, st);
 }
 
-// axis-0 pass of one kernel: W (+)= IFFT0(K FFT0(V)), rows [0, c0)
-int pass_axis0_single(eik_plan* p, const double2* V, const KDev& k, double2* W, bool accum, cudaStream_t st) {
+// axis-0 pass of a list of kernels: W_j (+)= IFFT0(K_j FFT0(V)), rows [0, c0)
+int pass_axis0_list(eik_plan* p, const double2* V, const KDev* const* ks, int n, double2* const* W, bool accum,
+                    cudaStream_t st) {
   const int64_t H = p->H, M1 = p->M[1];
   ColArgs a = col_defaults(p);
   a.nlines = M1 * H;
@@ -937,11 +948,17 @@ int pass_axis0_single(eik_plan* p, const double2* V, const KDev& k, double2* W, 
   a.fold_M1 = (int)M1;
   a.fold_k1base = 0;
   a.fold_f0 = p->fold_f0;
-  a.ks[0] = kspec_of(p, k);
-  a.out[0] = W;
-  a.n_comp = 1;
+  for (int j = 0; j < n; ++j) {
+    a.ks[j] = kspec_of(p, *ks[j]);
+    a.out[j] = W[j];
+  }
+  a.n_comp = n;
   a.accum = accum ? 1 : 0;
   return launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, 1, st);
+}
+int pass_axis0_single(eik_plan* p, const double2* V, const KDev& k, double2* W, bool accum, cudaStream_t st) {
+  const KDev* kk = &k;
+  return pass_axis0_list(p, V, &kk, 1, &W, accum, st);
 }
 
 struct StreamEpi {
@@ -1321,11 +1338,15 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       if ((rc2 = pass_planes_inplace(p, false, d_nodes, in->n_nodes, nullptr, V1, st))) return rc2;
       e.phi_raw = o_S ? o_S : (o_phi ? o_phi : p->work.as<double>());
       if ((rc2 = pass_axis0_single(p, V1, *p->kdist[p->k_exp], W1, false, st))) return rc2;
-      if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, e.phi_raw))) return rc2;
+      RawOut ro;
+      ro.n = 1;
+      ro.dest[0] = e.phi_raw;
+      if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, &ro))) return rc2;
       for (int d = 0; d < r.ngrad; ++d) {
         if (!o_g[d]) continue;
         if ((rc2 = pass_axis0_single(p, V1, *p->kdist[p->k_grad + d], W1, false, st))) return rc2;
-        if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, o_g[d]))) return rc2;
+        ro.dest[0] = o_g[d];
+        if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, &ro))) return rc2;
         e.grad[d] = o_g[d];
       }
       e.S = o_S;
@@ -1342,7 +1363,10 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
         if ((rc2 = pass_axis0_single(p, V1, *p->ksign[i], W1, i > 0, st))) return rc2;
       }
       e.mu_raw = o_mu ? o_mu : p->work.as<double>() + p->N;
-      if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, e.mu_raw))) return rc2;
+      RawOut rs;
+      rs.n = 1;
+      rs.dest[0] = e.mu_raw;
+      if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, &rs))) return rc2;
       e.mu = o_mu;
       e.mask = o_mask;
       if ((rc2 = mark(EIK_PASS_COL_SIGN, true))) return rc2;
@@ -1646,7 +1670,6 @@ int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const 
                           eik_plan** out) {
   if (!out || !counts || !taus || n_taus < 1) return fail(EIK_EVALIDATION, "null argument");
   *out = nullptr;
-  if (dim > 2) return fail(EIK_EVALIDATION, "the tau sweep is implemented for 1-D and 2-D grids");
   for (int i = 0; i < n_taus; ++i)
     if (!(taus[i] > 0)) return fail(EIK_EVALIDATION, "tau must be > 0");
   CK(cudaSetDevice(device));
@@ -1655,6 +1678,7 @@ int eik_plan_create_sweep(int dim, const int64_t* counts, double spacing, const 
   p->tau = taus[0];
   int rc = setup_geometry(p.get(), dim, counts, spacing);
   if (rc) return rc;
+  if (p->D == 3) init_fold(p.get(), 0, p->M[1]);
   CK(p->work.ensure((size_t)p->M[0] * p->lines * sizeof(double2)));
   for (int i = 0; i < n_taus; ++i) {
     if ((rc = add_kernel(p.get(), p->ksweep, KT_EXP, 0, false, 1.0, p->work.as<double2>(), nullptr, taus[i]))) return rc;
@@ -1689,10 +1713,40 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
     for (int i = 0; i < nt; ++i) outs[i] = p->stage.as<double>() + (int64_t)i * p->N;
   }
   const int64_t ce = p->comp_elems();
-  CK(p->comp.ensure((size_t)std::min(nt, MAXC) * ce * sizeof(double2)));
+  // 3-D: chunks of <= 4 taus (one component buffer each next to the spectrum V)
+  const int chunk = p->D == 3 ? std::min(MAXC, 4) : MAXC;
+  CK(p->comp.ensure((size_t)std::min(nt, chunk) * ce * sizeof(double2)));
   CK(p->counter.ensure(sizeof(unsigned long long)));
   CK(cudaMemsetAsync(p->counter.p, 0, sizeof(unsigned long long), st));
-  int rc = prep_nodes(p, d_nodes, nullptr, n_nodes, 1, p->N, p->c[0], p->c[1], p->rowid, p->cols,
+  int rc;
+  if (p->D == 3) {
+    // planes pass once (impulse DFT along axis 2 + FFT along axis 1); every chunk
+    // of taus reuses V: axis-0 pass with the chunk's exp spectra, inverse along
+    // axis 1, raw row pass with S_j = -tau_j log phi_j
+    CK(p->vin.ensure((size_t)ce * sizeof(double2)));
+    double2* V = p->vin.as<double2>();
+    if ((rc = pass_planes_inplace(p, false, d_nodes, n_nodes, nullptr, V, st))) return rc;
+    Roles r0;
+    std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
+    for (int t0 = 0; t0 < nt; t0 += chunk) {
+      const int nc = std::min(chunk, nt - t0);
+      const KDev* kk[MAXC];
+      double2* W[MAXC];
+      RawOut ro;
+      ro.n = nc;
+      for (int j = 0; j < nc; ++j) {
+        kk[j] = p->ksweep[t0 + j].get();
+        W[j] = p->comp.as<double2>() + (int64_t)j * ce;
+        ro.dest[j] = outs[t0 + j];
+        ro.tau[j] = p->taus[t0 + j];
+      }
+      if ((rc = pass_axis0_list(p, V, kk, nc, W, false, st))) return rc;
+      RowArgs ra{};
+      ra.uf_count = p->counter.as<unsigned long long>();
+      if ((rc = pass_finish(p, W, r0, p->c[0], p->M[1], 1, ra, st, nomark, nullptr, &ro))) return rc;
+    }
+  } else {
+  rc = prep_nodes(p, d_nodes, nullptr, n_nodes, 1, p->N, p->c[0], p->c[1], p->rowid, p->cols,
                       p->rowptr, st);
   if (rc) return rc;
   // impulse DFT once; every chunk of <= 8 taus reuses T
@@ -1754,6 +1808,7 @@ int eik_run_sweep(eik_plan* p, const int64_t* nodes, int64_t n_nodes, double* co
     ra.row0 = 0;
     ra.row_end = ra.rows;
     if ((rc = launch_row(p->L[1] - 1, ra, 1, st))) return rc;
+  }
   }
   if (host_out)
     for (int i = 0; i < nt; ++i)

@@ -141,6 +141,19 @@ def s_fft(ps, grid, cfg, convolver=None, kernel_hat=None) -> ScalarField:
     return ScalarField(grid, _run_phi_family(ps, grid, cfg, want_s=True, what="phi"))
 
 
+def r_exact(points, grid) -> ScalarField:
+    """Exact distance to the nearest source (R/distance.py:155-168): the KD-tree
+    nearest-neighbour distance at every node.  Host-side evaluation tool of the
+    experiment protocols, not part of the convolution path."""
+    from scipy.spatial import cKDTree
+
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    if pts.shape[1] != grid.dim:
+        raise ValidationError("point dimensionality does not match grid")
+    dist, _ = cKDTree(pts).query(grid.node_coords(), k=1)
+    return ScalarField(grid, np.asarray(dist, dtype=np.float64))
+
+
 def error_bound(cfg, k: int) -> float:
     return log_bound(cfg.tau, k)
 

@@ -79,13 +79,13 @@ class TauSweep:
     The GPU analogue of the kernel reuse in R/experiments.py:74-109 (one
     FftConvolver shared by the nine tau values of the Example-1 protocol):
     here the impulse DFT and forward column FFT are shared, each tau adds one
-    cached exp spectrum, one inverse and its own -tau log phi epilogue.
+    cached exp spectrum, one inverse and its own -tau log phi epilogue.  3-D
+    grids share the planes pass (impulse DFT along axis 2, FFT along axis 1)
+    and run the axis-0 pass in chunks of four tau values.
     Unchecked: S is NaN where phi <= 0 and the total count is returned.
     """
 
     def __init__(self, grid, taus, device=0):
-        if len(grid.counts) > 2:
-            raise ValidationError("the tau sweep is implemented for 1-D and 2-D grids")
         self.grid = grid
         self.taus = [float(t) for t in taus]
         self.plan = _native.SweepPlan(len(grid.counts), grid.counts, grid.spacing, self.taus, device)

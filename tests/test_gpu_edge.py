@@ -158,6 +158,24 @@ def test_tau_sweep_matches_single_tau_runs(cuda_ok):
         assert (np.abs(S - ref["S"])[keep] / np.maximum(np.abs(ref["S"][keep]), 1.0)).max() <= 1e-9
 
 
+def test_tau_sweep_3d_matches_single_tau_runs(cuda_ok):
+    """3-D sweep (shared planes pass, chunks of four tau values): every S_tau is
+    bit-identical to the single-tau pipeline and within T1 of the oracle."""
+    from paper_1112_3010_b200 import engine
+
+    grid = _grid((20, 24, 18))
+    nodes = np.sort(rng_for(17).choice(grid.num_nodes, 90, replace=False))
+    taus = [0.75, 1.0, 1.5, 2.0, 3.0]  # two chunks
+    outs, n_uf = engine.TauSweep(grid, taus).run_host(nodes)
+    assert len(outs) == 5
+    for tau, S in zip(taus, outs):
+        single = engine.DistanceTransform(grid, tau, grad=False).run_host(nodes)["S"]
+        assert np.array_equal(S, single, equal_nan=True)
+        ref = orc.run_config_unchecked(nodes, grid.counts, 1.0, tau)
+        keep = ref["phi"] >= 1e-5 * ref["phi"].max()
+        assert (np.abs(S - ref["S"])[keep] / np.maximum(np.abs(ref["S"][keep]), 1.0)).max() <= 1e-9
+
+
 @pytest.mark.parametrize("counts", [(40, 33), (17, 16, 15), (64,)])
 def test_gpu_classify_matches_scipy_fill(cuda_ok, counts):
     """GPU nearest-unflagged fill + rounding == reference classify (scipy EDT), bit for bit."""

@@ -95,3 +95,25 @@ def test_vertex_area_normals_sum_to_zero():
     assert np.abs(w.sum(axis=0)).max() < 1e-9
     # outward: flux of the position field equals 3 * volume > 0
     assert np.einsum("ij,ij->", v, w) > 0
+
+
+def test_percentage_error_and_r_exact_match_reference_definitions():
+    """metrics.percentage_error (R/metrics.py:46-72) and distance.r_exact
+    (R/distance.py:155-168) against their definitions written out."""
+    from paper_1112_3010_b200 import GridSpec, ScalarField
+    from paper_1112_3010_b200.distance import r_exact
+    from paper_1112_3010_b200.metrics import Report, percentage_error
+
+    grid = GridSpec((0.0, -1.0), 0.5, (7, 9))
+    rng = np.random.default_rng(4)
+    pts = grid.node_coords()[rng.choice(grid.num_nodes, 6, replace=False)]
+    ex = r_exact(pts, grid)
+    brute = np.sqrt(((grid.node_coords()[:, None, :] - pts[None, :, :]) ** 2).sum(-1)).min(1)
+    assert np.array_equal(ex.values, brute)
+    comp = ScalarField(grid, ex.values * (1.0 + 0.01 * rng.standard_normal(grid.num_nodes)))
+    st = percentage_error(comp, ex)
+    inc = brute > 0
+    per = 100.0 * np.abs(comp.values - brute)[inc] / brute[inc]
+    assert st.included == int(inc.sum()) == grid.num_nodes - 6 and st.total == grid.num_nodes
+    assert st.mean == per.mean() and st.maximum == per.max() and st.paper_mean == per.sum() / grid.num_nodes
+    assert '"experiment": "x"' in Report("x", {"a": 1}, [{"b": 2}]).to_json()
