@@ -39,7 +39,7 @@ CONFIG_TEXT = {
           "(metric counts grid points x taus)",
     "C4": "3D 1024^3 perturbed icosphere (501,762 vertices, vector-area normals), tau=0.75: S + grad S + degree sign; "
           "slab-decomposed, exchange fused into the passes as NVLink peer stores (--exchange nccl: NCCL "
-          "all-to-all) (512^3 with scaled surface on fewer than 4 GPUs: memory)",
+          "all-to-all); 1 GPU: eik_run's streamed schedule; 2 GPUs: streamed slab schedule over NCCL",
 }
 
 
@@ -56,8 +56,7 @@ def parse():
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="C4 slab exchange: fused peer stores (p2p) or NCCL all_to_all_single")
     ap.add_argument("--c4-size", type=int, default=0,
-                    help="C4 grid edge (default 1024 on >= 4 GPUs, else 512: one fixed size for a strong-scaling "
-                         "series, pass e.g. --c4-size 512 at every N)")
+                    help="C4 grid edge (default 1024 at every rank count; smaller grids scale the surface)")
     ap.add_argument("--dry-run", action="store_true",
                     help="no device work: launch the ranks (gloo), build each rank's shard and print the line "
                          "skeleton (tests the multi-rank plumbing on CPU)")
@@ -787,14 +786,20 @@ def bench_c4(a):
     dev = torch.device("cuda", local)
     from paper_1112_3010_b200 import workloads as wl
     from paper_1112_3010_b200.slab import (CudaSlabExecutor, connect_p2p, fill_masks_emulated, fill_rank,
-                                           local_nodes, nccl_exchange, run_rank, run_rank_p2p, stream_barrier)
+                                           local_nodes, nccl_exchange, run_rank, run_rank_p2p, run_rank_streamed,
+                                           stream_barrier)
 
-    n = a.c4_size or (1024 if world >= 4 else 512)
+    # one fixed problem (1024^3) at every rank count: on fewer than 4 ranks the
+    # fused schedule's 9 spectrum / component slots per rank exceed 180 GB, so
+    # those run the streamed slab schedule (one V pair, one W pair, NCCL all-to-all)
+    n = a.c4_size or 1024
+    streamed = (n >= 1024 and world < 4) or os.environ.get("EIK_C4_STREAMED") == "1"
     d = wl.c4(a.seed, n=n)
     grid = d["grid"]
     t_plan = time.perf_counter()
-    p2p = a.exchange == "p2p"
-    ex = CudaSlabExecutor(grid, d["tau"], world, rank, grad=True, sign=True, device=local, p2p=p2p)
+    p2p = a.exchange == "p2p" and not streamed
+    ex = CudaSlabExecutor(grid, d["tau"], world, rank, grad=True, sign=True, device=local, p2p=p2p,
+                          streamed=streamed)
     t_plan = time.perf_counter() - t_plan
     ln, _ = local_nodes(d["nodes"], ex.layout)
     lsn, lsw = local_nodes(d["sign_nodes"], ex.layout, d["sign_weights"])
@@ -813,10 +818,10 @@ def bench_c4(a):
         run_schedule = run_p2p
         exchange = None
     elif dist:
-        run_schedule = run_rank
+        run_schedule = run_rank_streamed if streamed else run_rank
         exchange = nccl_exchange(dist)
     else:
-        run_schedule = run_rank
+        run_schedule = run_rank_streamed if streamed else run_rank
 
         def exchange(send, recv):
             for s_, r_ in zip(send, recv):
@@ -878,7 +883,9 @@ def bench_c4(a):
                        "nodes": int(d["nodes"].size),
                        "parallelism": parallelism("C4", world, over) + (
                            " (exchange fused into the passes: NVLink peer stores, 2 stream barriers; mask halo "
-                           "planes point-to-point)" if p2p else " (NCCL all-to-all)"),
+                           "planes point-to-point)" if p2p else
+                           " (streamed: one input / one component at a time, NCCL all-to-all)" if streamed else
+                           " (NCCL all-to-all)"),
                        "exchange_bytes_per_step": int(9 * 16 * L.buf * world * (world - 1) / world) if world > 1 else 0,
                        "l2": "working set >> L2", "plan_build_s": round(t_plan, 3)},
             "e2e": {"value": grid.num_nodes * ke / (e2e_ms / 1e3), "unit": "grid_points/s",

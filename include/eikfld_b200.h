@@ -183,6 +183,26 @@ int eik_slab_p2p_init(eik_plan* plan, int world, int rank, int64_t c0_local, int
                       int64_t* arena_bytes, void* ipc_handle);
 int eik_slab_p2p_connect(eik_plan* plan, void* const* peer_arenas, const void* ipc_handles);
 
+/* Streamed slab schedule: one input and one component at a time, so a rank
+ * holds one V and one W buffer pair instead of one per input and component
+ * (C4 at 1024^3 on 2 GPUs; eik_run does the same on one GPU).  eik_slab_planes_one:
+ * the planes pass of the distance input (group 0) or of flux input `input` in
+ * 0..2 (group 1; weights is the full [3][n_nodes] array).  eik_slab_axis0_one:
+ * W (+)= IFFT0(K FFT0(V)) for one kernel (0 exp, 1..3 gradient, 4..6 degree);
+ * accumulate != 0 adds into W (the degree sums its three inputs).
+ * eik_slab_finish_raw: inverse along axis 1 + c2r of ONE component into the
+ * scaled real-space field raw_out (no epilogue).  eik_slab_epilogue: the
+ * elementwise epilogue over the rank's n_local nodes: S = -tau log phi_raw,
+ * out->grad[a] (holding the raw numerators) /= phi_raw, mu = -mu_raw / 4 pi,
+ * mask = rint(mu) >= 1 -- the operations of the fused row epilogue. */
+int eik_slab_planes_one(eik_plan* plan, int group, int input, const int64_t* nodes, int64_t n_nodes,
+                        const double* weights, int64_t c0_local, int64_t ks, double* v_out, void* stream);
+int eik_slab_axis0_one(eik_plan* plan, int kernel, const double* v_in, int64_t k1_begin, int64_t ks, double* w_out,
+                       int accumulate, void* stream);
+int eik_slab_finish_raw(eik_plan* plan, double* w, int64_t c0_local, int64_t ks, double* raw_out, void* stream);
+int eik_slab_epilogue(eik_plan* plan, int64_t n_local, const double* phi_raw, const double* mu_raw,
+                      const eik_outputs* out, void* stream);
+
 /* Flagged-node fill of a slab rank's sign mask (the classify step of
  * R/sign.py:179-195, which eik_run performs internally): eik_slab_finish
  * classifies every owned node by its own mu; this call then gives each owned

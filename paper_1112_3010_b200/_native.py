@@ -96,7 +96,16 @@ def lib():
             L.eik_ifft_window.argtypes = [C.c_int, _i64p, C.c_void_p, C.c_void_p, _i64p, _i64p, C.c_void_p,
                                           C.c_void_p, C.c_uint32, C.c_int, C.c_void_p]
             L.eik_cmul.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p]
+            L.eik_slab_planes_one.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                                              C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+            L.eik_slab_axis0_one.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                             C.c_int, C.c_void_p]
+            L.eik_slab_finish_raw.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+            L.eik_slab_epilogue.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(Outputs),
+                                            C.c_void_p]
             L.eik_last_error.restype = C.c_char_p
+            for name in ("eik_slab_planes_one", "eik_slab_axis0_one", "eik_slab_finish_raw", "eik_slab_epilogue"):
+                getattr(L, name).restype = C.c_int
             for name in ("eik_plan_create", "eik_plan_destroy", "eik_plan_info", "eik_run", "eik_convolve",
                          "eik_version", "eik_pass_times", "eik_plan_create_slab", "eik_slab_planes",
                          "eik_slab_axis0", "eik_slab_finish", "eik_plan_create_sweep", "eik_run_sweep",
@@ -113,6 +122,7 @@ def exported_symbols():
             "eik_convolve", "eik_slab_planes", "eik_slab_axis0", "eik_slab_finish", "eik_pass_times",
             "eik_plan_create_sweep", "eik_run_sweep", "eik_classify", "eik_slab_p2p_init", "eik_slab_p2p_connect",
             "eik_dd_plan_create", "eik_dd_plan_destroy", "eik_dd_run", "eik_slab_fill",
+            "eik_slab_planes_one", "eik_slab_axis0_one", "eik_slab_finish_raw", "eik_slab_epilogue",
             "eik_fftn", "eik_fft_pair", "eik_ifft_window", "eik_cmul",
             "eik_last_error", "eik_version"]
 
@@ -208,6 +218,26 @@ class Plan:
         out.d_underflow_count = _ptr(d_count)
         check(lib().eik_slab_finish(self._h, wa, int(c0_local), int(ks), C.byref(out), SLAB_P2P if p2p else 0,
                                     stream))
+
+    # -- streamed slab schedule: one input / one component at a time
+    def slab_planes_one(self, group, inp, nodes, weights, c0_local, ks, v_out, stream=None):
+        check(lib().eik_slab_planes_one(self._h, int(group), int(inp), _ptr(nodes), int(nodes.shape[0]),
+                                        _ptr(weights), int(c0_local), int(ks), _ptr(v_out), stream))
+
+    def slab_axis0_one(self, kernel, v_in, k1_begin, ks, w_out, accumulate=False, stream=None):
+        check(lib().eik_slab_axis0_one(self._h, int(kernel), _ptr(v_in), int(k1_begin), int(ks), _ptr(w_out),
+                                       1 if accumulate else 0, stream))
+
+    def slab_finish_raw(self, w, c0_local, ks, raw_out, stream=None):
+        check(lib().eik_slab_finish_raw(self._h, _ptr(w), int(c0_local), int(ks), _ptr(raw_out), stream))
+
+    def slab_epilogue(self, n_local, phi_raw, mu_raw, *, S=None, grad=(None, None, None), mu=None, mask=None,
+                      underflow=None, stream=None):
+        out = Outputs()
+        out.S, out.mu, out.mask, out.underflow = (_ptr(x) for x in (S, mu, mask, underflow))
+        for d in range(3):
+            out.grad[d] = _ptr(grad[d]) if d < len(grad) else None
+        check(lib().eik_slab_epilogue(self._h, int(n_local), _ptr(phi_raw), _ptr(mu_raw), C.byref(out), stream))
 
     def slab_fill(self, ext_nodes, e0, e1, own0, c0_local, mask_ext, mask_own, stream=None):
         check(lib().eik_slab_fill(self._h, _ptr(ext_nodes), int(ext_nodes.shape[0]), int(e0), int(e1), int(own0),

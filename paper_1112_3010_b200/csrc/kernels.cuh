@@ -471,7 +471,8 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
         const int n = LN::in_idx(t, r);
         if (valid && n < a.n_out) {
           double2* dst = comp_dst(a, j, item, l, n);
-          *dst = a.accum ? cadd(*dst, y[r]) : y[r];
+          if (a.accum) *dst = cadd(*dst, y[r]);
+          else *dst = y[r];
         }
       }
     }
@@ -825,13 +826,22 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
           kapply_all<LN>(v, kn, a.ks[j], t, mir);
         }
         fft_line<LN, true>(v, t, xb, tws);
+        if (a.accum) {  // uniform: the streamed sign group adds into W
 #pragma unroll
-        for (int r = 0; r < LN::EPT; ++r) {
-          if (LN::L > 0 && LN::upper_in(r)) continue;
-          const int n = LN::in_idx(t, r);
-          if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) {
-            double2* dst = comp_dst(a, j, item, l, n);
-            *dst = a.accum ? cadd(*dst, v[r]) : v[r];
+          for (int r = 0; r < LN::EPT; ++r) {
+            if (LN::L > 0 && LN::upper_in(r)) continue;
+            const int n = LN::in_idx(t, r);
+            if (valid && n < a.n_out) {
+              double2* dst = comp_dst(a, j, item, l, n);
+              *dst = cadd(*dst, v[r]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < LN::EPT; ++r) {
+            if (LN::L > 0 && LN::upper_in(r)) continue;
+            const int n = LN::in_idx(t, r);
+            if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) *comp_dst(a, j, item, l, n) = v[r];
           }
         }
       }

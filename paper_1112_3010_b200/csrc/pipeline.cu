@@ -667,15 +667,18 @@ struct PeerBlk {
   int64_t cstride = 0;
 };
 
+// in0 / nin: the sign group's inputs [in0, in0 + nin) only (streamed schedules; nin < 0: all)
 int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
-                int64_t c0loc, int64_t ks, double2* const* V, cudaStream_t st, const PeerBlk* pb = nullptr) {
+                int64_t c0loc, int64_t ks, double2* const* V, cudaStream_t st, const PeerBlk* pb = nullptr,
+                int in0 = 0, int nin = -1) {
   const int64_t H = p->H, c1 = p->c[1], c2 = p->c[2];
   DevBuf& rid = sg ? p->srowid : p->rowid;
   DevBuf& cl = sg ? p->scols : p->cols;
   DevBuf& rp = sg ? p->srowptr : p->rowptr;
   int rc = prep_nodes(p, nodes, off, K, B, c0loc * c1 * c2, c0loc * c1, c2, rid, cl, rp, st);
   if (rc) return rc;
-  const int n_in = sg ? 3 : 1;
+  const int n_in = nin >= 0 ? nin : (sg ? 3 : 1);
+  if (sg && w) w += (int64_t)in0 * K;
   static const bool rowdft = [] {
     const char* e = std::getenv("EIK_ROWDFT");
     return !(e && e[0] == '0');
@@ -724,7 +727,7 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
   ColArgs a = col_defaults(p);
   a.rowptr = rp.as<int64_t>();
   a.cols = cl.as<int32_t>();
-  a.n_in = sg ? 3 : 1;
+  a.n_in = n_in;
   for (int i = 0; i < 3; ++i) a.w[i] = (sg && i < a.n_in) ? w + (int64_t)i * K : nullptr;
   a.last_shift = p->lmax - p->L[2];
   a.last_mask = p->M[2] - 1;
@@ -932,21 +935,24 @@ int pass_planes_inplace(eik_plan* p, bool sg, const int64_t* nodes, int64_t K, c
 
 // axis-0 pass of a list of kernels: W_j (+)= IFFT0(K_j FFT0(V)), rows [0, c0)
 int pass_axis0_list(eik_plan* p, const double2* V, const KDev* const* ks, int n, double2* const* W, bool accum,
-                    cudaStream_t st) {
+                    cudaStream_t st, int64_t k1b = 0, int64_t kslab = -1) {
   const int64_t H = p->H, M1 = p->M[1];
+  const int64_t kk = kslab < 0 ? M1 : kslab;  // lines of the k1 slab [k1b, k1b + kk)
+  if (k1b < p->k1_begin || k1b + kk > p->k1_begin + p->k1_count)
+    return fail(EIK_EVALIDATION, "k1 slab not covered by the plan's kernel spectra");
   ColArgs a = col_defaults(p);
-  a.nlines = M1 * H;
+  a.nlines = kk * H;
   a.n_valid = p->c[0];
   a.n_out = p->c[0];
   a.n_in = 1;
   a.din[0] = V;
-  a.din_es = M1 * H;
-  a.din_item = (int64_t)p->c[0] * M1 * H;
-  a.out_es = M1 * H;
-  a.out_item = (int64_t)p->c[0] * M1 * H;
+  a.din_es = kk * H;
+  a.din_item = (int64_t)p->c[0] * kk * H;
+  a.out_es = kk * H;
+  a.out_item = (int64_t)p->c[0] * kk * H;
   a.fold_H = (int)H;
   a.fold_M1 = (int)M1;
-  a.fold_k1base = 0;
+  a.fold_k1base = k1b;
   a.fold_f0 = p->fold_f0;
   for (int j = 0; j < n; ++j) {
     a.ks[j] = kspec_of(p, *ks[j]);
@@ -1650,6 +1656,89 @@ int eik_slab_finish(eik_plan* p, double* const* w, int64_t c0_local, int64_t ks,
   std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
   if ((rc = pass_finish(p, W.data(), r, c0_local, ks, 1, ra, st, nomark))) return rc;
   if (flags & EIK_SYNC) CK(cudaStreamSynchronize(st));
+  return EIK_OK;
+}
+
+// ---- streamed slab schedule: one input / one component at a time, so a rank
+// holds one V and one W buffer pair instead of one per input and component
+// (C4 at 1024^3 on 2 GPUs).  Kernels: 0 = exp, 1..3 = gradient, 4..6 = degree.
+
+int eik_slab_planes_one(eik_plan* p, int group, int input, const int64_t* nodes, int64_t n_nodes,
+                        const double* weights, int64_t c0_local, int64_t ks, double* v_out, void* stream) {
+  if (!p || !v_out) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  Roles r;
+  int rc = slab_roles(p, r);
+  if (rc) return rc;
+  if (group == 1 && (!r.sign || input < 0 || input > 2 || !weights))
+    return fail(EIK_EVALIDATION, "sign input outside 0..2, no weights, or a plan without sign kernels");
+  if (group == 0 && !r.phi) return fail(EIK_EVALIDATION, "plan was built without the distance kernels");
+  if (ks < 1 || p->M[1] % ks || (ks & (ks - 1)) || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
+  double2* V[3] = {(double2*)v_out, nullptr, nullptr};
+  return pass_planes(p, group == 1, nodes, nullptr, n_nodes, 1, weights, c0_local, ks, V,
+                     static_cast<cudaStream_t>(stream), nullptr, group == 1 ? input : 0, 1);
+}
+
+static const KDev* slab_kernel(const eik_plan* p, int kernel) {
+  if (kernel == 0) return p->k_exp >= 0 ? p->kdist[p->k_exp].get() : nullptr;
+  if (kernel >= 1 && kernel <= 3) return p->k_grad >= 0 ? p->kdist[p->k_grad + kernel - 1].get() : nullptr;
+  if (kernel >= 4 && kernel <= 6) return (int)p->ksign.size() == 3 ? p->ksign[kernel - 4].get() : nullptr;
+  return nullptr;
+}
+
+int eik_slab_axis0_one(eik_plan* p, int kernel, const double* v_in, int64_t k1_begin, int64_t ks, double* w_out,
+                       int accumulate, void* stream) {
+  if (!p || !v_in || !w_out) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  if (p->D != 3) return fail(EIK_EVALIDATION, "the slab API is for 3-D grids");
+  const KDev* k = slab_kernel(p, kernel);
+  if (!k) return fail(EIK_EVALIDATION, "kernel not in the plan (0 exp, 1..3 gradient, 4..6 degree)");
+  if (ks < 1 || p->M[1] % ks || k1_begin < 0 || k1_begin + ks > p->M[1]) return fail(EIK_EVALIDATION, "bad slab geometry");
+  double2* W = (double2*)w_out;
+  return pass_axis0_list(p, (const double2*)v_in, &k, 1, &W, accumulate != 0, static_cast<cudaStream_t>(stream),
+                         k1_begin, ks);
+}
+
+int eik_slab_finish_raw(eik_plan* p, double* w, int64_t c0_local, int64_t ks, double* raw_out, void* stream) {
+  if (!p || !w || !raw_out) return fail(EIK_EVALIDATION, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  CK(cudaSetDevice(p->device));
+  if (p->D != 3) return fail(EIK_EVALIDATION, "the slab API is for 3-D grids");
+  if (ks < 1 || p->M[1] % ks || c0_local < 1) return fail(EIK_EVALIDATION, "bad slab geometry");
+  Roles r;
+  RawOut ro;
+  ro.n = 1;
+  ro.dest[0] = raw_out;
+  double2* W = (double2*)w;
+  RowArgs ra{};
+  std::function<int(int, bool)> nomark = [](int, bool) { return EIK_OK; };
+  return pass_finish(p, &W, r, c0_local, ks, 1, ra, static_cast<cudaStream_t>(stream), nomark, nullptr, &ro);
+}
+
+int eik_slab_epilogue(eik_plan* p, int64_t n_local, const double* phi_raw, const double* mu_raw,
+                      const eik_outputs* out, void* stream) {
+  if (!p || !out || n_local < 1) return fail(EIK_EVALIDATION, "null argument");
+  CK(cudaSetDevice(p->device));
+  StreamEpi e{};
+  e.N = n_local;
+  e.tau = p->tau;
+  e.phi_raw = const_cast<double*>(phi_raw);
+  e.mu_raw = const_cast<double*>(mu_raw);
+  if (phi_raw) {
+    e.S = out->S;
+    e.phi_out = out->phi;
+    e.uf = out->underflow;
+    e.uf_count = out->d_underflow_count;
+    for (int d = 0; d < 3; ++d) e.grad[d] = out->grad[d];
+  }
+  if (mu_raw) {
+    e.mu = out->mu;
+    e.mask = out->mask;
+  }
+  stream_epilogue_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(e);
+  CK(cudaGetLastError());
   return EIK_OK;
 }
 

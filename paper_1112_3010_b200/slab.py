@@ -170,6 +170,67 @@ def run_rank(ex, exchange, nodes, sign_nodes=None, sign_weights=None):
     return ex.finish()
 
 
+def run_rank_streamed(ex, exchange, nodes, sign_nodes=None, sign_weights=None):
+    """One rank of the streamed slab schedule (executor built with streamed=True):
+    one input and one component at a time through ONE V pair and ONE W pair, so
+    C4 at 1024^3 fits two GPUs.  Same all-to-all count as run_rank (one per
+    input, one per component); every component returns as a raw real-space field
+    and the epilogue runs elementwise at the end."""
+    ex.planes_one(0, 0, nodes, None)
+    exchange(ex.V_send, ex.V_recv)
+    for j in range(ex.n_dist):
+        ex.axis0_one(j, accumulate=False)
+        exchange(ex.W, ex.W_recv)
+        ex.finish_raw(j)
+    if ex.sign and sign_nodes is not None:
+        for i in range(3):
+            ex.planes_one(1, i, sign_nodes, sign_weights)
+            exchange(ex.V_send, ex.V_recv)
+            ex.axis0_one(4 + i, accumulate=i > 0)
+        exchange(ex.W, ex.W_recv)
+        ex.finish_raw("mu")
+    return ex.epilogue()
+
+
+def run_emulated_streamed(executors, node_lists):
+    """All ranks of the streamed schedule in one process, phase by phase
+    (exchanges as block copies); for testing on one device."""
+    G = len(executors)
+
+    def swap(send, recv):
+        for r in range(G):
+            dst = recv(executors[r])[0].view(G, -1)
+            for g in range(G):
+                dst[g].copy_(send(executors[g])[0].view(G, -1)[r])
+
+    def vswap():
+        swap(lambda e: e.V_send, lambda e: e.V_recv)
+
+    def wswap():
+        swap(lambda e: e.W, lambda e: e.W_recv)
+
+    for r, ex in enumerate(executors):
+        ex.planes_one(0, 0, node_lists[r][0], None)
+    vswap()
+    for j in range(executors[0].n_dist):
+        for ex in executors:
+            ex.axis0_one(j, accumulate=False)
+        wswap()
+        for ex in executors:
+            ex.finish_raw(j)
+    if executors[0].sign and node_lists[0][1] is not None:
+        for i in range(3):
+            for r, ex in enumerate(executors):
+                ex.planes_one(1, i, node_lists[r][1], node_lists[r][2])
+            vswap()
+            for ex in executors:
+                ex.axis0_one(4 + i, accumulate=i > 0)
+        wswap()
+        for ex in executors:
+            ex.finish_raw("mu")
+    return [ex.epilogue() for ex in executors]
+
+
 def nccl_exchange(dist):
     """exchange(send, recv) = one all_to_all_single per buffer (equal peer blocks)."""
 
@@ -273,7 +334,7 @@ def run_emulated(executors, node_lists):
 class CudaSlabExecutor:
     """CUDA passes of one rank (libeikfld_b200 slab API) with torch device buffers."""
 
-    def __init__(self, grid, tau, world, rank, *, grad=True, sign=True, device=0, p2p=False):
+    def __init__(self, grid, tau, world, rank, *, grad=True, sign=True, device=0, p2p=False, streamed=False):
         import torch
 
         from . import _native
@@ -297,7 +358,16 @@ class CudaSlabExecutor:
         self.n_dist = 1 + (3 if grad else 0)
         n_comp = self.n_dist + (1 if sign else 0)
         self.p2p = p2p
+        self.streamed = streamed
         self.N_local = L.c0loc * L.plane_nodes
+        if streamed:
+            # one V pair and one W pair; the returned component reuses V_send (dead by then)
+            if p2p:
+                raise ValidationError("the streamed slab schedule uses the all-to-all exchange")
+            self.V_send, self.V_recv, self.W = [mk()], [mk()], [mk()]
+            self.W_recv = self.V_send
+            self._out = None
+            return
         if p2p:
             # one arena per rank in the receive layout; the passes store into the
             # owners' arenas, so no send / staging buffers exist at all
@@ -336,6 +406,52 @@ class CudaSlabExecutor:
             self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, None, self._stream(), p2p=True)
         else:
             self.plan.slab_planes(group, nd, wt, L.c0loc, L.ks, self.V_send[:3 if group else 1], self._stream())
+
+    # -- streamed schedule (run_rank_streamed)
+    def _dev(self, x, dt):
+        import torch
+
+        if x is None or isinstance(x, torch.Tensor):
+            return x
+        return torch.as_tensor(np.ascontiguousarray(x, dtype=dt), device=self.dev)
+
+    def _outputs(self):
+        import torch
+
+        if self._out is None:
+            f = lambda: torch.empty(self.N_local, dtype=torch.float64, device=self.dev)  # noqa: E731
+            out = {"S": f(), "underflow": torch.empty(self.N_local, dtype=torch.uint8, device=self.dev)}
+            if self.grad:
+                out["grad"] = [f() for _ in range(3)]
+            if self.sign:
+                out["mu"] = f()
+                out["mask"] = torch.empty(self.N_local, dtype=torch.uint8, device=self.dev)
+            self._out = out
+        return self._out
+
+    def planes_one(self, group, inp, nodes, weights):
+        L = self.layout
+        nd, wt = self._dev(nodes, np.int64), self._dev(weights, np.float64)
+        self._keep = (nd, wt)
+        self.plan.slab_planes_one(group, inp, nd, wt, L.c0loc, L.ks, self.V_send[0], self._stream())
+
+    def axis0_one(self, kernel, accumulate=False):
+        L = self.layout
+        self.plan.slab_axis0_one(kernel, self.V_recv[0], L.k1_begin, L.ks, self.W[0], accumulate, self._stream())
+
+    def finish_raw(self, which):
+        """Component `which` (0 = phi -> S buffer, 1..3 = gradient numerators, "mu") back to real space, raw."""
+        L = self.layout
+        out = self._outputs()
+        dest = out["mu"] if which == "mu" else (out["S"] if which == 0 else out["grad"][which - 1])
+        self.plan.slab_finish_raw(self.W_recv[0], L.c0loc, L.ks, dest, self._stream())
+
+    def epilogue(self):
+        out = self._outputs()
+        self.plan.slab_epilogue(self.N_local, out["S"], out.get("mu"), S=out["S"], grad=out.get("grad", (None,) * 3),
+                                mu=out.get("mu"), mask=out.get("mask"), underflow=out["underflow"],
+                                stream=self._stream())
+        return out
 
     def axis0(self, group):
         L = self.layout

@@ -91,6 +91,58 @@ class NumpySlabExecutor:
         return out
 
 
+class NumpyStreamedSlabExecutor(NumpySlabExecutor):
+    """The streamed schedule (slab.run_rank_streamed) on CPU ranks: one V pair
+    and one W pair, one input / one component at a time, raw components plus
+    an elementwise epilogue."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        L = self.layout
+        mk = lambda: np.zeros((L.world, L.block), dtype=np.complex128)  # noqa: E731
+        self.V_send, self.V_recv, self.W = [mk()], [mk()], [mk()]
+        self.W_recv = self.V_send
+        self.raw = {}
+
+    def planes_one(self, group, inp, nodes, weights):
+        L = self.layout
+        c0, c1, c2 = L.counts
+        M0, M1, M2 = L.padded
+        g = np.zeros(L.c0loc * c1 * c2)
+        np.add.at(g, nodes, 1.0 if not group else weights[inp])
+        t = np.fft.fft(np.fft.rfft(g.reshape(L.c0loc, c1, c2), n=M2, axis=2), n=M1, axis=1)
+        for dest in range(L.world):
+            self.V_send[0][dest] = t[:, dest * L.ks:(dest + 1) * L.ks, :].reshape(-1)
+
+    def axis0_one(self, kernel, accumulate=False):
+        L = self.layout
+        c0, M0 = L.counts[0], L.padded[0]
+        k = self.kd[kernel] if kernel < 4 else self.ksg[kernel - 4]
+        x = np.fft.fft(self.V_recv[0].reshape(c0, L.ks, L.H), n=M0, axis=0)
+        y = np.fft.ifft(k * x, axis=0)[:c0].reshape(L.world, L.block)
+        if accumulate:
+            self.W[0] += y
+        else:
+            self.W[0][:] = y
+
+    def finish_raw(self, which):
+        L = self.layout
+        c0, c1, c2 = L.counts
+        M0, M1, M2 = L.padded
+        a = self.W_recv[0].reshape(L.world, L.c0loc, L.ks, L.H).transpose(1, 0, 2, 3).reshape(L.c0loc, M1, L.H)
+        a = np.fft.ifft(a, axis=1)[:, :c1, :]
+        self.raw[which] = np.fft.irfft(a, n=M2, axis=2)[:, :, :c2].reshape(-1).copy()
+
+    def epilogue(self):
+        phi = self.raw[0]
+        out = {"phi": phi, "S": -self.tau * np.log(np.where(phi > 0, phi, np.nan))}
+        if self.grad:
+            out["grad"] = [self.raw[j] / phi for j in (1, 2, 3)]
+        if self.sign and "mu" in self.raw:
+            out["mu"] = -self.raw["mu"] / (4.0 * math.pi)
+        return out
+
+
 class NumpyP2PSlabExecutor(NumpySlabExecutor):
     """The fused peer-to-peer schedule on CPU ranks: every rank's receive arena
     is a shared-memory segment laid out like the CUDA arena ([4 V slots][W

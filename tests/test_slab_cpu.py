@@ -40,13 +40,16 @@ def _worker(rank, world, port, outdir, p2p=False):
     import torch
     import torch.distributed as dist
 
-    from paper_1112_3010_b200.slab import local_nodes, run_rank, run_rank_p2p
-    from slab_numpy import NumpyP2PSlabExecutor, NumpySlabExecutor
+    from paper_1112_3010_b200.slab import local_nodes, run_rank, run_rank_p2p, run_rank_streamed
+    from slab_numpy import NumpyP2PSlabExecutor, NumpySlabExecutor, NumpyStreamedSlabExecutor
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ex = (NumpyP2PSlabExecutor if p2p else NumpySlabExecutor)(COUNTS, H_SP, TAU, world, rank)
+    streamed = p2p == "streamed"
+    p2p = p2p is True
+    cls = NumpyStreamedSlabExecutor if streamed else (NumpyP2PSlabExecutor if p2p else NumpySlabExecutor)
+    ex = cls(COUNTS, H_SP, TAU, world, rank)
     nodes, snodes, sw = _inputs()
     ln, _ = local_nodes(nodes, ex.layout)
     lsn, lsw = local_nodes(snodes, ex.layout, sw)
@@ -68,16 +71,17 @@ def _worker(rank, world, port, outdir, p2p=False):
             rt = torch.from_numpy(r.view(np.float64))
             dist.all_to_all_single(rt, torch.from_numpy(np.ascontiguousarray(s).view(np.float64)))
 
-    out = run_rank(ex, exchange, ln, lsn, lsw)
+    out = (run_rank_streamed if streamed else run_rank)(ex, exchange, ln, lsn, lsw)
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), S=out["S"], phi=out["phi"], mu=out["mu"],
              gx=out["grad"][0], gy=out["grad"][1], gz=out["grad"][2])
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("p2p", [False, True, "streamed"])
 @pytest.mark.parametrize("world", [2])
 def test_slab_schedule_world2_gloo(world, p2p):
-    """NCCL-style all-to-all schedule and the fused peer-store schedule."""
+    """NCCL-style all-to-all schedule, the fused peer-store schedule and the
+    streamed (one input / one component at a time) schedule."""
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, _free_port(), d, p2p), nprocs=world, join=True)
         parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]

@@ -47,6 +47,49 @@ def test_emulated_slab_bit_identical(cuda_ok, world, p2p):
         assert np.array_equal(got[f"g{a}"], ref["grad"][a], equal_nan=True)
 
 
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_emulated_streamed_slab_matches_eik_run(cuda_ok, world, monkeypatch):
+    """The streamed slab schedule (one V pair, one W pair per rank): S and grad S
+    bit-identical to eik_run, mu to rounding (it sums its three inputs after the
+    inverse transforms), masks equal after the fill; and bit-identical in every
+    field to eik_run's own streamed schedule."""
+    import torch
+
+    from paper_1112_3010_b200 import GridSpec, engine, workloads
+    from paper_1112_3010_b200.slab import CudaSlabExecutor, fill_masks_emulated, local_nodes, run_emulated_streamed
+
+    grid = GridSpec((-15.5, -15.5, -15.5), 1.0, (32, 32, 32))
+    tau = 0.75
+    v, f = workloads.perturbed_sphere(0, freq=12, radius=10.0)
+    surf = workloads.surface_from_mesh(v, f)
+    rng = np.random.Generator(np.random.PCG64(5))
+    nodes = np.sort(rng.choice(grid.num_nodes, 400, replace=False))
+    dt = engine.DistanceTransform(grid, tau, grad=True, sign=True)
+    sn, sw = dt.sign_inputs(surf)
+    ref = dt.run_host(nodes, sign_nodes=sn, sign_weights=sw)
+    monkeypatch.setenv("EIK_STREAM3D", "1")
+    ref_s = dt.run_host(nodes, sign_nodes=sn, sign_weights=sw)
+    monkeypatch.delenv("EIK_STREAM3D")
+
+    exs = [CudaSlabExecutor(grid, tau, world, r, streamed=True) for r in range(world)]
+    lists = []
+    for ex in exs:
+        ln, _ = local_nodes(nodes, ex.layout)
+        lsn, lsw = local_nodes(sn, ex.layout, sw)
+        lists.append((ln, lsn, lsw))
+    outs = run_emulated_streamed(exs, lists)
+    fill_masks_emulated(exs, outs, sn, hd=1)
+    torch.cuda.synchronize()
+    got = {k: torch.cat([o[k] for o in outs]).cpu().numpy() for k in ("S", "mu", "mask")}
+    assert np.array_equal(got["S"], ref["S"], equal_nan=True)
+    assert np.abs(got["mu"] - ref["mu"]).max() <= 1e-12
+    assert np.array_equal(got["mu"], ref_s["mu"])
+    assert np.array_equal(got["mask"], ref["mask"])
+    for a in range(3):
+        ga = torch.cat([o["grad"][a] for o in outs]).cpu().numpy()
+        assert np.array_equal(ga, ref["grad"][a], equal_nan=True)
+
+
 def test_p2p_slab_repeat_and_validation(cuda_ok):
     """Two consecutive steps through the same arenas agree; geometry is checked."""
     import torch
