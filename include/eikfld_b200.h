@@ -69,7 +69,8 @@ extern "C" {
 #define EIK_PASS_COL_SIGN 2 /* fused column kernel, sign group */
 #define EIK_PASS_LINES 3    /* 3-D inverse along axis 1 */
 #define EIK_PASS_ROW 4      /* c2r along the last axis + epilogue */
-#define EIK_NPASS 5
+#define EIK_PASS_COL_KERNEL 5 /* the distance group's column / axis-0 kernel alone (inside EIK_PASS_COL) */
+#define EIK_NPASS 6
 
 typedef struct eik_plan eik_plan;
 

@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(os.path.dirname(os.path.abs
 EIK_OK, EIK_EVALIDATION, EIK_EUNDERFLOW, EIK_ECUDA = 0, 1, 2, 3
 FIELD_PHI, FIELD_S, FIELD_GRAD, FIELD_HESS, FIELD_WINDING, FIELD_DEGREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 HOST_INPUTS, HOST_OUTPUTS, SYNC, CHECK_UNDERFLOW, PROFILE, SLAB_P2P, ASYNC = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
-PASS_NAMES = ("prep", "col", "col_sign", "lines", "row")
+PASS_NAMES = ("prep", "col", "col_sign", "lines", "row", "col_kernel")
 
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)

@@ -33,6 +33,17 @@ namespace eik {
 #ifndef EIK_TW_POW
 #define EIK_TW_POW 1
 #endif
+// Timing-only debug switches (results are wrong with any of them on; used by
+// tools/ablate.sh to split a kernel's time into its FP64 / exchange / memory parts)
+#ifndef EIK_DBG_NODFT
+#define EIK_DBG_NODFT 0
+#endif
+#ifndef EIK_DBG_NOTW
+#define EIK_DBG_NOTW 0
+#endif
+#ifndef EIK_DBG_NOXCHG
+#define EIK_DBG_NOXCHG 0
+#endif
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -167,17 +178,6 @@ __device__ __forceinline__ void bfly_levels(double2* x) {
 
 // In-register R-point DFT (natural order in/out), radix-2 DIT, R <= 16.
 // HALF_IN: a[R/2..R) are known zero (not read).
-// Timing-only debug switches (results are wrong with any of them on; used by
-// tools/ablate.sh to split a kernel's time into its FP64 / exchange / memory parts)
-#ifndef EIK_DBG_NODFT
-#define EIK_DBG_NODFT 0
-#endif
-#ifndef EIK_DBG_NOTW
-#define EIK_DBG_NOTW 0
-#endif
-#ifndef EIK_DBG_NOXCHG
-#define EIK_DBG_NOXCHG 0
-#endif
 template <int R, bool INV, bool HALF_IN>
 __device__ __forceinline__ void dft(double2* a) {
   if constexpr (EIK_DBG_NODFT) return;
@@ -377,7 +377,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int b = t + g * LN::TPL;
-    if constexpr (NS > 1) {
+    if constexpr (NS > 1 && !EIK_DBG_NOTW) {
       const int k = b & (NS - 1);
       bool done = false;
       if constexpr (LN::st_quarter(INV, S) && G == 1 && R == 16) {
@@ -433,7 +433,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
     }
     dft<R, INV, HALF_IN && S == 0>(&v[g * R]);
   }
-  if constexpr (S + 1 < LN::NST) {
+  if constexpr (S + 1 < LN::NST && !EIK_DBG_NOXCHG) {
     double2* sm = xb.cur();
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -548,8 +548,15 @@ __device__ __forceinline__ void f4k_twiddle_row(double2 (&v)[16], int x, const T
 
 // XB::sync() is the barrier over the threads of this line: the CTA when its
 // lines are interleaved across all warps, a named barrier for line-major CTAs
-template <bool HALF_IN, class XB>
-__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw) {
+// HOOK: called by every thread right after the transform's first CTA-wide
+// barrier (the column kernels issue their pending TMA output stores there).
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <bool HALF_IN, class XB, class HOOK = NoHook>
+__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw,
+                                            const HOOK& hook = HOOK()) {
   constexpr int P = Line4K::PITCH;
   double2* sm = xb.b0;
   const int g = t >> 4, x = t & 15;
@@ -558,6 +565,7 @@ __device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& x
   f4k_twiddle_t<false>(v, t, tw);
   if constexpr (!EIK_DBG_NOXCHG) {
   xb.sync();  // every thread is done with the buffer (previous transform)
+  hook();
 #pragma unroll
   for (int r = 0; r < 16; ++r) sm[r * P + t] = v[r];
   xb.sync();
@@ -577,8 +585,9 @@ __device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& x
   dft<16, false, false>(v);                             // over j: v[b] = X[g + 16 x + 256 b]
 }
 
-template <class XB>
-__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw) {
+template <class XB, class HOOK = NoHook>
+__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw,
+                                            const HOOK& hook = HOOK()) {
   constexpr int P = Line4K::PITCH;
   double2* sm = xb.b0;
   const int g = t >> 4, x = t & 15;
@@ -599,6 +608,7 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& x
 #pragma unroll
   for (int m = 0; m < 16; ++m) row[x + 16 * m] = v[m];
   xb.sync();
+  hook();
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = sm[r * P + t];  // thread t = n2: v[k1]
   xb.sync();  // buffer free again: the next transform may write any row
@@ -609,12 +619,13 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& x
 
 // Full transform of the line held in v (layouts documented above).
 // HALF_IN (forward only): input elements >= M/2 are zero and their registers are not read.
-template <class LN, bool INV, bool HALF_IN = false, class XB>
-__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw) {
+template <class LN, bool INV, bool HALF_IN = false, class XB, class HOOK = NoHook>
+__device__ __forceinline__ void fft_line(double2 (&v)[LN::EPT], int t, XB& xb, const TwSrc& tw,
+                                         const HOOK& hook = HOOK()) {
   static_assert(!(INV && HALF_IN), "input pruning is a forward-transform feature");
   if constexpr (LN::FOUR_STEP) {
-    if constexpr (INV) f4k_inverse(v, t, xb, tw);
-    else f4k_forward<HALF_IN>(v, t, xb, tw);
+    if constexpr (INV) f4k_inverse(v, t, xb, tw, hook);
+    else f4k_forward<HALF_IN>(v, t, xb, tw, hook);
   } else {
     stages_from<LN, INV, 0, HALF_IN && (LN::L > 0)>(v, t, xb, tw);
   }

@@ -225,6 +225,11 @@ struct ColArgs {
   // kernels when k1 > M1/2.  fold_H = 0: lines are read as they are (2-D).
   int fold_H, fold_M1;
   int64_t fold_k1base, fold_f0;
+  // TMA output stores (4096-point four-step kernels, set by the launcher): component j
+  // leaves through a shared-memory tile [row][LPC lines] as boxes of 2*LPC doubles x 256
+  // rows of umap[j], a [item][row][2 * nlines doubles] view of out[j]
+  int tstore;
+  CUtensorMap umap[MAXC];
   // OUT_COMPS: add the component into its destination instead of overwriting it
   // (streamed 3-D sign group: one flux input at a time, W += IFFT0(K_i FFT0(V_i)))
   int accum;
@@ -620,6 +625,22 @@ struct TmCfg {
   static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
+  // TMA output stores (ColArgs::tstore): the staging tile [M/2 rows][LPC lines] and its
+  // hand-over flag after the base layout, 128-byte aligned
+  // (A/B switch, default off.  Measured on the B200 with the hand-over built
+  // without any extra CTA barrier: distance column kernel 0.330 -> 0.322 ms, but the
+  // C2 step 0.829 -> 0.887 ms.  Writing the tile alone costs 15 us of the 61 us the
+  // direct stores cost (tools/gpu_ablate.sh), yet the engine reads the tile back in
+  // 32-byte rows, a quarter of the shared-memory width per cycle, so the time
+  // returns on the shared-memory pipe the exchanges already saturate;
+  // tools/micro/tma_store_probe.cu: 2765 clocks per 64 KB tile with the SM idle.)
+#ifndef EIK_TSTORE
+#define EIK_TSTORE 0
+#endif
+  static constexpr bool TSTORE = EIK_TSTORE && F4K && LPC == 2;
+  static constexpr size_t TSTORE_OFF = (SMEM_BYTES + 127) & ~size_t(127);
+  static constexpr size_t TSTORE_TILE = (size_t)(LN::M / 2) * LPC * sizeof(double2);
+  static constexpr size_t SMEM_TSTORE_BYTES = TSTORE_OFF + 128 + TSTORE_TILE + 32;
 };
 
 // L2 prefetch for the CTA that runs one resident wave later (linear CTA index
@@ -715,6 +736,9 @@ __device__ __forceinline__ void unstage_dense(double2 (&v)[LN::EPT], const doubl
 #ifndef EIK_DBG_NOST
 #define EIK_DBG_NOST 0
 #endif
+#ifndef EIK_DBG_STAGEONLY
+#define EIK_DBG_STAGEONLY 0
+#endif
 template <int L, int IN, int OUT, bool HALF>
 __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpcx(L, OUT)>::MINB)
     col_tmem_kernel(const __grid_constant__ ColArgs a) {
@@ -749,6 +773,17 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   const TwSrc tws{sts, twq, L, ttw, ttw2};
   const int tiles = (int)a.tiles;
   const int total = tiles * (int)a.items;  // < 2^31 (launcher)
+  // TMA output stores: fill counter and the fill thread 0 still has to hand over
+  int ts_seq = 0;
+  if constexpr (TC::TSTORE && OUT == OUT_COMPS) {
+    if (a.tstore && threadIdx.x == 0) {
+      char* sbase = reinterpret_cast<char*>(smem);
+      const uint32_t mis = smem_u32(sbase + TC::TSTORE_OFF) & 127u;
+      volatile int* w = reinterpret_cast<volatile int*>(sbase + TC::TSTORE_OFF + (mis ? 128u - mis : 0u) + TC::TSTORE_TILE);
+      w[0] = 0;
+      w[1] = 0;
+    }
+  }
 
 #pragma unroll 1
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -807,6 +842,65 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
         const int n = LN::in_idx(t, r);
         if (valid && n < a.n_out) *comp_dst(a, 0, item, l, n) = v[r];
       }
+    } else if (TC::TSTORE && OUT == OUT_COMPS && a.tstore) {
+      // Outputs through shared memory and TMA.  Fill s of the staging tile (one per
+      // component) is handed to the TMA engine by thread 0 right after the next
+      // CTA-wide barrier (every thread's tile writes precede it), i.e. inside the
+      // next transform; before fill s + 1 thread 0 waits until the engine has read
+      // fill s and publishes that through a shared flag.  No extra CTA barrier.
+      if constexpr (TC::TSTORE && OUT == OUT_COMPS) {
+        char* sbase = reinterpret_cast<char*>(smem);
+        const uint32_t mis = smem_u32(sbase + TC::TSTORE_OFF) & 127u;
+        double2* stg = reinterpret_cast<double2*>(sbase + TC::TSTORE_OFF + (mis ? 128u - mis : 0u));
+        // hand-over words after the tile: [0] fills whose tile has been read, [1] a fill
+        // is pending, [2..4] its component, tile and item (thread 0's bookkeeping)
+        volatile int* freed = reinterpret_cast<volatile int*>(reinterpret_cast<char*>(stg) + TC::TSTORE_TILE);
+        auto hook = [&]() {
+          if (threadIdx.x == 0 && freed[1]) {
+            for (int y = 0; y < a.n_out; y += 256)
+              tma_store_3d(&a.umap[freed[2]], stg + y * LPC, freed[3] * LPC * 2, y, freed[4]);
+            bulk_commit();
+            freed[1] = 0;
+          }
+        };
+        if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
+        else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
+        fft_line<LN, false, HALF>(v, t, xb, tws, hook);
+        tmem_put(ta, v);
+        if (valid) kprefetch_all<TC>(a.ks[0], lk, t, bx);
+#pragma unroll 1
+        for (int j = 0; j < a.n_comp; ++j) {
+          tmem_get(ta, v);
+          if (valid) {
+            double kn[LN::EPT];
+            kload_all<TC>(kn, a.ks[j], lk, t, bx);
+            if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], lk, t, bx);
+            kapply_all<LN>(v, kn, a.ks[j], t, mir);
+          }
+          fft_line<LN, true>(v, t, xb, tws, hook);
+          // the tile is free once the engine has read the previous fill
+          ++ts_seq;
+          if (threadIdx.x == 0) {
+            bulk_wait_read0();
+            *freed = ts_seq;
+          }
+          __syncwarp();
+          while (*freed < ts_seq) {
+          }
+#pragma unroll
+          for (int r = 0; r < LN::EPT; ++r) {
+            if (LN::L > 0 && LN::upper_in(r)) continue;
+            stg[LN::in_idx(t, r) * LPC + line] = v[r];
+          }
+          fence_proxy_async_smem();
+          if (threadIdx.x == 0) {
+            freed[1] = 1;
+            freed[2] = j;
+            freed[3] = bx;
+            freed[4] = item;
+          }
+        }
+      }
     } else {
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
@@ -837,13 +931,40 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
             }
           }
         } else {
+#if EIK_DBG_STAGEONLY
+          // timing probe: the component goes to a shared-memory tile [row][line] only
+          double2* stg = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) + ((TC::SMEM_BYTES + 127) & ~size_t(127)));
+#pragma unroll
+          for (int r = 0; r < LN::EPT; ++r) {
+            if (LN::L > 0 && LN::upper_in(r)) continue;
+            const int n = LN::in_idx(t, r);
+            if (n < LN::M / 2) stg[n * LPC + line] = v[r];
+          }
+#else
 #pragma unroll
           for (int r = 0; r < LN::EPT; ++r) {
             if (LN::L > 0 && LN::upper_in(r)) continue;
             const int n = LN::in_idx(t, r);
             if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) *comp_dst(a, j, item, l, n) = v[r];
           }
+#endif
         }
+      }
+    }
+  }
+  if constexpr (TC::TSTORE && OUT == OUT_COMPS) {
+    if (a.tstore) {  // the last fill leaves after one more barrier; the tile stays valid until it is read
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        char* sbase = reinterpret_cast<char*>(smem);
+        const uint32_t mis = smem_u32(sbase + TC::TSTORE_OFF) & 127u;
+        double2* stg = reinterpret_cast<double2*>(sbase + TC::TSTORE_OFF + (mis ? 128u - mis : 0u));
+        volatile int* w = reinterpret_cast<volatile int*>(reinterpret_cast<char*>(stg) + TC::TSTORE_TILE);
+        if (w[1]) {
+          for (int y = 0; y < a.n_out; y += 256) tma_store_3d(&a.umap[w[2]], stg + y * LPC, w[3] * LPC * 2, y, w[4]);
+          bulk_commit();
+        }
+        bulk_wait_read0();
       }
     }
   }

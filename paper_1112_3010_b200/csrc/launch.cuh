@@ -1,7 +1,9 @@
 // Shared host-side helpers for the launcher translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
+#include <cstdint>
 #include <cstdlib>
 #include <string>
 
@@ -48,6 +50,34 @@ inline int sm_count() {
   return cached[dev];
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// [item][row][2 * nlines doubles] view of a column-pass output (row stride out_es
+// complex, item stride out_item complex), boxes of 2 * lpc doubles x 256 rows
+inline bool encode_out_map(CUtensorMap* m, double2* out, const ColArgs& a, int64_t items, int lpc) {
+  auto fn = tensor_map_encoder();
+  if (!fn || !out) return false;
+  if (((uintptr_t)out & 15) || a.out_es < a.nlines) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * a.nlines), (cuuint64_t)a.n_out, (cuuint64_t)items};
+  const cuuint64_t strides[2] = {(cuuint64_t)a.out_es * 16, (cuuint64_t)(items > 1 ? a.out_item : a.out_es * a.n_out) * 16};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * lpc), 256u, 1u};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // EIK_PERSIST: 0 / 1 force one CTA per tile / persistent CTAs everywhere; unset: per-kernel default
 inline int persist_mode() {
   static const int mode = [] {
@@ -63,7 +93,8 @@ template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_persistent(const ColArgs& a, int64_t items, cudaStream_t st) {
   using C = TmCfg<L, tm_lpcx(L, OUT)>;
   auto k = col_tmem_kernel<L, IN, OUT, HALF>;
-  CK(prep_kernel_attr(k, C::SMEM_BYTES));
+  const size_t smem_max = C::SMEM_BYTES + ((EIK_DBG_STAGEONLY || C::TSTORE) && L == 12 ? 256 + (size_t)(C::LN::M / 2) * C::LPC * 16 : 0);
+  CK(prep_kernel_attr(k, smem_max));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
   if (tiles <= 0 || items <= 0) return EIK_OK;
   // measured (B200): persistent C2 col 0.377 -> 0.361 ms, C5 5.52 -> 5.36 ms, but
@@ -73,11 +104,28 @@ int launch_tmem_persistent(const ColArgs& a, int64_t items, cudaStream_t st) {
   ColArgs b = a;
   b.tiles = tiles;
   b.items = items;
+  // TMA output stores (4096-point four-step distance kernels): plain own-buffer
+  // outputs only (no slab blocks, split rows or accumulation); EIK_TSTORE=0 at run time turns them off
+  b.tstore = 0;
+  size_t smem_tstore = 0;
+  if constexpr (C::TSTORE && OUT == OUT_COMPS) {
+    static const bool ts_on = [] {
+      const char* e = std::getenv("EIK_TSTORE");
+      return !(e && e[0] == '0');
+    }();
+    if (ts_on && !a.blk[0] && a.out_split_shift >= 30 && !a.accum && a.n_out <= C::LN::M / 2 && a.n_comp <= MAXC) {
+      b.tstore = 1;
+      for (int j = 0; j < a.n_comp && b.tstore; ++j)
+        if (!encode_out_map(&b.umap[j], a.out[j], a, items, C::LPC)) b.tstore = 0;
+      if (b.tstore) smem_tstore = C::SMEM_TSTORE_BYTES;
+    }
+  }
   const int64_t total = tiles * items;
   const int64_t wave = (int64_t)sm_count() * C::MINB;
   const int64_t grid = persist ? (total < wave ? total : wave) : total;
   if (total > 0x7fffffffLL) return fail(EIK_EVALIDATION, "too many column tiles in one launch");
-  k<<<(unsigned)grid, C::NT, C::SMEM_BYTES, st>>>(b);
+  const size_t smem_bytes = smem_tstore ? smem_tstore : (EIK_DBG_STAGEONLY ? smem_max : C::SMEM_BYTES);
+  k<<<(unsigned)grid, C::NT, smem_bytes, st>>>(b);
   CK(cudaGetLastError());
   return EIK_OK;
 }

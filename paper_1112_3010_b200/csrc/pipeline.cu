@@ -541,6 +541,11 @@ struct Roles {
   int n_comp() const { return n_dist() + (sign ? 1 : 0); }
 };
 
+// run_locked's profiling hook, visible to the pass functions (nullptr: not profiling)
+using MarkFn = std::function<int(int, bool)>;
+thread_local const MarkFn* g_mark = nullptr;
+int mark_pass(int pass, bool end) { return g_mark ? (*g_mark)(pass, end) : EIK_OK; }
+
 int set_components(const eik_plan* p, bool sign_group, const Roles& r, ColArgs& x, double2* const* W,
                    int64_t k1_offset_lines) {
   if (p->D == 3) {  // folded storage along axis 1: the kernels map pass lines to stored lines
@@ -636,8 +641,11 @@ int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, i
     a.out_es = p->rs();
     a.out_item = p->comp_elems();
     set_components(p, sg, r, a, W, 0);
-    return sg ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st)
-              : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st);
+    if (sg) return launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st);
+    int rcm;
+    if ((rcm = mark_pass(EIK_PASS_COL_KERNEL, false))) return rcm;
+    if ((rcm = launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st))) return rcm;
+    return mark_pass(EIK_PASS_COL_KERNEL, true);
   }
   ColArgs a = col_defaults(p);
   a.rowptr = rowptr;
@@ -768,8 +776,11 @@ int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks,
     a.blk_shift = pb->shift;
     a.blk_cstride = pb->cstride;
   }
-  return sg ? launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st)
-            : launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st);
+  if (sg) return launch_col<IN_DENSE, OUT_SUM, true>(p->L[0], a, B, st);
+  int rcm;
+  if ((rcm = mark_pass(EIK_PASS_COL_KERNEL, false))) return rcm;
+  if ((rcm = launch_col<IN_DENSE, OUT_COMPS, true>(p->L[0], a, B, st))) return rcm;
+  return mark_pass(EIK_PASS_COL_KERNEL, true);
 }
 
 // 3-D pass C (or the 2-D row pass): inverse along axis 1 (3-D only) + c2r along
@@ -1115,6 +1126,10 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     if (end) p->ev_used[pass] = true;
     return EIK_OK;
   };
+  struct MarkScope {  // the pass functions reach `mark` through g_mark while this run is on the stack
+    explicit MarkScope(const MarkFn* m) { g_mark = m; }
+    ~MarkScope() { g_mark = nullptr; }
+  } mark_scope(prof ? &mark : nullptr);
   // ---- inputs
   const int64_t* d_nodes = in->nodes;
   const int64_t* d_off = in->item_offsets;
