@@ -1372,9 +1372,12 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   };
   const int64_t obase = item * a.N + row * a.n_out;
 
+#ifndef EIK_DBG_ROW_NOST
+#define EIK_DBG_ROW_NOST 0
+#endif
   auto put = [&](double* dst, int r, double x0, double x1) {
     const int n = 2 * LN::in_idx(t, r);
-    if (!valid || n >= a.n_out) return;
+    if (!valid || n >= a.n_out || (EIK_DBG_ROW_NOST && a.n_comp < 100)) return;
     if (even) *reinterpret_cast<double2*>(dst + obase + n) = make_double2(x0, x1);
     else { dst[obase + n] = x0; if (n + 1 < a.n_out) dst[obase + n + 1] = x1; }
   };
