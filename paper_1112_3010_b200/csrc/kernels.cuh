@@ -306,9 +306,6 @@ __device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpe
   }
 }
 // L1 prefetch of this thread's EPT kernel-spectrum values (TMEM column kernel).
-#ifndef EIK_KPF
-#define EIK_KPF 1
-#endif
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 template <class CFG>
 __device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t, int64_t bx) {
@@ -643,38 +640,6 @@ struct TmCfg {
   static constexpr size_t SMEM_TSTORE_BYTES = TSTORE_OFF + 128 + TSTORE_TILE + 32;
 };
 
-// L2 prefetch for the CTA that runs one resident wave later (linear CTA index
-// + `ahead`, x fastest): its first global reads then hit L2 instead of DRAM.
-#ifndef EIK_L2PF
-#define EIK_L2PF 0
-#endif
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool cta_ahead(int ahead, int64_t& bx, int64_t& by) {
-  const int64_t lin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + ahead;
-  bx = lin % gridDim.x;
-  by = lin / gridDim.x;
-  return by < gridDim.y;
-}
-// dense column input of tile (bx, by): rows [0, n_valid) x LPC adjacent lines
-template <int LPC, int NT>
-__device__ __forceinline__ void prefetch_dense_tile(const ColArgs& a, int n_in, int ahead) {
-  int64_t bx, by;
-  if (!cta_ahead(ahead, bx, by)) return;
-  const int64_t l0 = bx * LPC;
-  if (l0 >= a.nlines) return;
-  for (int i = 0; i < n_in; ++i) {
-    const double2* base = a.din[i] + by * a.din_item + l0 * a.din_ls;
-    for (int r = threadIdx.x; r < a.n_valid; r += NT) {
-      const double2* p = base + (int64_t)r * a.din_es;
-      prefetch_l2(p);
-      if (a.din_ls == 1) prefetch_l2(p + LPC - 1);
-    }
-  }
-}
-
 // TMA tensor store (3-D box, shared -> global) and its bulk-group bookkeeping
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
@@ -684,43 +649,6 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
-
-// cp.async (16-byte, L2 only) global -> shared; src_bytes = 0 zero-fills
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// Stage this thread's non-zero elements of dense input `inp` (half-padded
-// line) into its private slots sbuf[c * NT + tid] without holding registers.
-template <class LN, int NT>
-__device__ __forceinline__ void stage_dense_async(double2* sbuf, const ColArgs& a, int t, int64_t l, int64_t item,
-                                                  int inp, bool valid) {
-  const double2* src = a.din[inp] + item * a.din_item + l * a.din_ls;
-  int c = 0;
-#pragma unroll
-  for (int r = 0; r < LN::EPT; ++r) {
-    if (LN::L > 0 && LN::upper_in(r)) continue;
-    const int e = LN::in_idx(t, r);
-    const bool ok = valid && e < a.n_valid;
-    cp_async16(sbuf + c * NT + threadIdx.x, ok ? src + (int64_t)e * a.din_es : a.din[inp], ok ? 16 : 0);
-    ++c;
-  }
-  cp_async_commit();
-}
-template <class LN, int NT>
-__device__ __forceinline__ void unstage_dense(double2 (&v)[LN::EPT], const double2* sbuf) {
-  cp_async_wait_all();
-  int c = 0;
-#pragma unroll
-  for (int r = 0; r < LN::EPT; ++r) {
-    if (LN::L > 0 && LN::upper_in(r)) continue;
-    v[r] = sbuf[c * NT + threadIdx.x];
-    ++c;
-  }
-}
 
 // Persistent: the grid is at most one resident wave of CTAs (launch_tmem_t);
 // each CTA fills its twiddle tables, allocates its TMEM columns and caches its
