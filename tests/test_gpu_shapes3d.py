@@ -1,6 +1,6 @@
 """Small and lopsided 3-D (and degenerate) grids against the oracle: the kernel
 spectra are stored folded along every axis, so every padded length from 1 to
-32 per axis, the Nyquist planes and the k1 mirror signs of the odd kernels
+64 per axis, the Nyquist planes and the k1 mirror signs of the odd kernels
 (gradient component 1, degree kernel 1) are exercised, through the fused and
 the streamed schedule."""
 
@@ -12,7 +12,7 @@ from conftest import rng_for
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(3, 2, 5), (2, 3, 2), (7, 1, 9), (1, 8, 3), (16, 2, 2), (5, 9, 1), (4, 4, 4), (9, 16, 5), (2, 2, 2)]
+SHAPES = [(3, 2, 5), (2, 3, 2), (7, 2, 9), (2, 8, 3), (16, 2, 2), (5, 9, 2), (4, 4, 4), (9, 16, 5), (2, 2, 2), (17, 3, 33)]
 
 
 @pytest.mark.parametrize("streamed", ["0", "1"])
