@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "bulk.cuh"
 #include "tmem.cuh"
 
 namespace eik {
@@ -341,29 +342,66 @@ __device__ __forceinline__ double2 st_tw(const TwSrc& tw, int k, int r) {
 
 // Exchange buffers of one line.  With NBUF = 2 consecutive exchanges alternate
 // between two buffers, so a stage needs one barrier (between its writes and
-// its reads) instead of two: writes of exchange k+2 cannot overtake reads of
-// exchange k because every thread passed the barrier of exchange k+1.
+// its reads): writes of exchange k+2 cannot overtake reads of exchange k
+// because every thread passed the barrier of exchange k+1.
 // SYNC selects the barrier that covers exactly the threads of one line:
 // 0 = the CTA (__syncthreads), 1 = the warp (lines of <= 32 threads, whole
 // lines per warp), 2 = named barrier `bar` over the NTH threads of the line
 // (line-major CTAs holding several lines), so lines of a CTA do not wait on
 // each other.
-template <int NBUF, int SYNC = 0, int NTH = 0>
+// With NBUF = 1 the second barrier of an exchange ("every thread has read the
+// buffer, it may be written again") is split-phase (EIK_XSPLIT): release()
+// after a thread's reads is one mbarrier arrival per warp and does not block;
+// acquire() before its next write into the buffer waits for that phase, which
+// by then (a radix stage of FP64 work later) has normally completed, so warps
+// start their butterflies as their own loads return instead of after the
+// slowest warp's.  `mb` is the line group's mbarrier (count = its warps).
+// Measured (B200): C2 step 0.819 -> 0.805 ms (column kernel 0.3225 -> 0.3176,
+// sign column kernel 0.2226 -> 0.2173, row 0.2601 -> 0.2564), C5 8.077 -> 8.021 ms,
+// TS 1.009 -> 0.994 ms; the register-resident col / lines kernels (ColCfg) keep
+// the blocking barrier (C3's axis-1 inverse measured 0.812 -> 0.829 ms with it).
+#ifndef EIK_XSPLIT
+#define EIK_XSPLIT 1
+#endif
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int NBUF, int SYNC = 0, int NTH = 0, bool SPLIT_OK = true>
 struct XBuf {
   double2* b0;
   double2* b1;
   int ph;
   int bar;
+  uint64_t* mb;
+  uint32_t par;
+  static constexpr bool SPLIT = EIK_XSPLIT && SPLIT_OK && NBUF == 1 && SYNC != 1;
   __device__ __forceinline__ double2* cur() const { return (NBUF == 2 && ph) ? b1 : b0; }
   __device__ __forceinline__ void sync() const {
     if constexpr (SYNC == 1) __syncwarp();
     else if constexpr (SYNC == 2) asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "n"(NTH) : "memory");
     else __syncthreads();
   }
-  __device__ __forceinline__ void done() {
-    if constexpr (NBUF == 2) ph ^= 1;
-    else sync();
+  // this thread has finished reading the buffer
+  __device__ __forceinline__ void release() {
+    if constexpr (NBUF == 2) {
+      ph ^= 1;
+    } else if constexpr (SPLIT) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(mb);
+    } else {
+      sync();
+    }
   }
+  // before this thread's next write into the buffer
+  __device__ __forceinline__ void acquire() {
+    if constexpr (SPLIT) {
+      mbar_wait(mb, par ^ 1u);
+      par ^= 1u;
+    }
+  }
+  __device__ __forceinline__ void done() { release(); }
+  // threads of one sync group's mbarrier (its warps arrive once per release)
+  __host__ __device__ static constexpr int group_warps(int cta_threads) { return (SYNC == 2 ? NTH : cta_threads) / 32; }
 };
 
 // One Stockham stage S of direction INV, followed (if not last) by the
@@ -434,6 +472,7 @@ __device__ __forceinline__ void stage(double2 (&v)[LN::EPT], int t, XB& xb, cons
     dft<R, INV, HALF_IN && S == 0>(&v[g * R]);
   }
   if constexpr (S + 1 < LN::NST && !EIK_DBG_NOXCHG) {
+    xb.acquire();
     double2* sm = xb.cur();
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -555,7 +594,7 @@ struct NoHook {
 };
 
 template <bool HALF_IN, class XB, class HOOK = NoHook>
-__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw,
+__device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, XB& xb, const TwSrc& tw,
                                             const HOOK& hook = HOOK()) {
   constexpr int P = Line4K::PITCH;
   double2* sm = xb.b0;
@@ -564,11 +603,11 @@ __device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& x
   dft<16, false, HALF_IN>(v);  // over n1: v[k1], thread t = n2
   f4k_twiddle_t<false>(v, t, tw);
   if constexpr (!EIK_DBG_NOXCHG) {
-  xb.sync();  // every thread is done with the buffer (previous transform)
-  hook();
+  xb.acquire();  // every thread is done with the buffer (previous transform)
 #pragma unroll
   for (int r = 0; r < 16; ++r) sm[r * P + t] = v[r];
   xb.sync();
+  hook();
 #pragma unroll
   for (int m = 0; m < 16; ++m) v[m] = row[x + 16 * m];  // row k1 = g, n2 = x + 16 m
   }
@@ -581,12 +620,13 @@ __device__ __forceinline__ void f4k_forward(double2 (&v)[16], int t, const XB& x
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = row[x * 17 + j];  // lane x = a
+  xb.release();  // (the next transform may write any row once every warp is here)
   }
   dft<16, false, false>(v);                             // over j: v[b] = X[g + 16 x + 256 b]
 }
 
 template <class XB, class HOOK = NoHook>
-__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& xb, const TwSrc& tw,
+__device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, XB& xb, const TwSrc& tw,
                                             const HOOK& hook = HOOK()) {
   constexpr int P = Line4K::PITCH;
   double2* sm = xb.b0;
@@ -595,7 +635,8 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& x
   dft<16, true, false>(v);  // over b: v[j], lane x = a
   f4k_twiddle_row<true>(v, x, tw);
   if constexpr (!EIK_DBG_NOXCHG) {
-  __syncwarp();  // the row is only touched by this half-warp since the last CTA barrier
+  xb.acquire();  // the previous transform's CTA-wide reads of this row are done
+  __syncwarp();
 #pragma unroll
   for (int j = 0; j < 16; ++j) row[x * 17 + j] = v[j];
   __syncwarp();
@@ -611,7 +652,7 @@ __device__ __forceinline__ void f4k_inverse(double2 (&v)[16], int t, const XB& x
   hook();
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = sm[r * P + t];  // thread t = n2: v[k1]
-  xb.sync();  // buffer free again: the next transform may write any row
+  xb.release();  // buffer free again once every warp is here: the next transform may write any row
   }
   f4k_twiddle_t<true>(v, t, tw);
   dft<16, true, false>(v);  // over k1: v[i] = x[t + 256 i]

@@ -114,8 +114,9 @@ struct ColCfg {
   // ping-pong exchange buffers (one barrier per exchange instead of two) where
   // they were measured to pay off without costing occupancy (C5-sized lines)
   static constexpr int NBUF = ((L == 10 || L == 11) && (2 * LPC * LN::SMEM + LN::TWQ) * 16 <= 200 * 1024) ? 2 : 1;
-  using XB = XBuf<NBUF, group_sync(IL, LPC, TPL0), IL * TPL0>;
-  static constexpr size_t SMEM_BYTES = ((size_t)NBUF * LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
+  using XB = XBuf<NBUF, group_sync(IL, LPC, TPL0), IL * TPL0, false>;
+  static constexpr size_t MB_OFF = ((size_t)NBUF * LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
+  static constexpr size_t SMEM_BYTES = MB_OFF + 128;  // + the split-phase exchange mbarriers
 };
 // Row kernels (c2r / r2c along the contiguous last axis): complex lines of
 // length 2^LH = M_last/2, quarter table at the resolution of M_last.
@@ -165,7 +166,8 @@ struct RowCfg {
 #endif
   static constexpr size_t FEED_BYTES = (size_t)LPC * (LN::M + 1) * sizeof(double2) + LPC * sizeof(uint64_t);
   static constexpr bool FEED = FEED_WANT && (BASE_BYTES + FEED_BYTES + 16) * MINB <= 227 * 1024;
-  static constexpr size_t SMEM_BYTES = BASE_BYTES + (FEED ? FEED_BYTES + 16 : 0);
+  static constexpr size_t MB_OFF = (BASE_BYTES + (FEED ? FEED_BYTES + 16 : 0) + 15) & ~size_t(15);
+  static constexpr size_t SMEM_BYTES = MB_OFF + 128;  // + the split-phase exchange mbarriers
 };
 
 // Kernel spectrum reference.  Real/imaginary spectra are stored transposed and
@@ -241,6 +243,31 @@ struct ColArgs {
   int blk_shift;
   int64_t blk_cstride;
 };
+
+
+// Split-phase exchange barriers (XBuf::acquire / release): mbarrier `group` of the
+// CTA's block at mbs, one per sync group; call before the kernel's first __syncthreads().
+template <class XB>
+__device__ __forceinline__ void xb_setup(XB& xb, uint64_t* mbs, int group, int ngroups, int cta_threads) {
+  xb.mb = mbs + group;
+  xb.par = 0u;
+  if constexpr (XB::SPLIT) {
+    if ((int)threadIdx.x < ngroups) mbar_init(mbs + threadIdx.x, (uint32_t)XB::group_warps(cta_threads));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+}
+constexpr size_t XB_MBAR_BYTES = 128;  // up to 16 sync groups per CTA
+
+// Streaming (evict-first) stores for data written once and read by a later
+// kernel (EIK_CS: 1 = component spectra U_j of the TMEM column kernels, 2 = also
+// the row pass's outputs)
+#ifndef EIK_CS
+#define EIK_CS 0
+#endif
+__device__ __forceinline__ void store_u(double2* dst, double2 x) {
+  if constexpr (EIK_CS >= 1) __stcs(dst, x);
+  else *dst = x;
+}
 
 // Destination of output row n of component j (own buffer or a peer's block).
 __device__ __forceinline__ double2* comp_dst(const ColArgs& a, int j, int64_t item, int64_t l, int n) {
@@ -435,6 +462,8 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
   typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line / CC::IL};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
+  xb_setup(xb, reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + CC::MB_OFF), line / CC::IL, LPC / CC::IL,
+           CC::NT);
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
@@ -621,7 +650,8 @@ struct TmCfg {
   static constexpr int WPT_ALL = WPT + (TWC ? 64 : 0) + (TWI ? 64 : 0);
   static constexpr int NEED = (NT / 128) * WPT_ALL;
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr size_t SMEM_BYTES = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
+  static constexpr size_t MB_OFF = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2) + 16;
+  static constexpr size_t SMEM_BYTES = MB_OFF + 128;  // + the split-phase exchange mbarriers
   // TMA output stores (ColArgs::tstore): the staging tile [M/2 rows][LPC lines] and its
   // hand-over flag after the base layout, 128-byte aligned
   // (A/B switch, default off.  Measured on the B200 with the hand-over built
@@ -680,6 +710,8 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   double2* twq = smem + LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
   uint32_t* slot = reinterpret_cast<uint32_t*>(sts + LN::ST_SIZE);
+  xb_setup(xb, reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + TC::MB_OFF), line / TC::IL, LPC / TC::IL,
+           TC::NT);
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
   const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the twiddle tables
@@ -768,7 +800,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       for (int r = 0; r < LN::EPT; ++r) {
         if (LN::L > 0 && LN::upper_in(r)) continue;
         const int n = LN::in_idx(t, r);
-        if (valid && n < a.n_out) *comp_dst(a, 0, item, l, n) = v[r];
+        if (valid && n < a.n_out) store_u(comp_dst(a, 0, item, l, n), v[r]);
       }
     } else if (TC::TSTORE && OUT == OUT_COMPS && a.tstore) {
       // Outputs through shared memory and TMA.  Fill s of the staging tile (one per
@@ -873,7 +905,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
           for (int r = 0; r < LN::EPT; ++r) {
             if (LN::L > 0 && LN::upper_in(r)) continue;
             const int n = LN::in_idx(t, r);
-            if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) *comp_dst(a, j, item, l, n) = v[r];
+            if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) store_u(comp_dst(a, j, item, l, n), v[r]);
           }
 #endif
         }
@@ -955,6 +987,8 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line / CC::IL};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
+  xb_setup(xb, reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + CC::MB_OFF), line / CC::IL, LPC / CC::IL,
+           CC::NT);
   if constexpr (L >= 2) twq_fill(twq, L, a.tw, a.lmax);
   st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
@@ -1109,6 +1143,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + RC::TWQ;
+  xb_setup(xb, reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + RC::MB_OFF), line, LPC, RC::NT);
   twq_fill(twq, LQ, tw, lmax);
   st_fill<LN>(sts, tw, lmax);
   __syncthreads();
@@ -1122,6 +1157,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT) row_r2c_kernel(const __grid_co
   fft_line<LN, false>(v, t, xb, tws);
   // natural-order spectrum Z into shared memory (the buffer the last exchange
   // did not use), then split into X[k], k in [0, MH]
+  xb.acquire();
   double2* sm = xb.cur();
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) sm[LN::pad(LN::out_idx(t, r))] = v[r];
@@ -1219,6 +1255,7 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   typename RC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line};
   double2* twq = smem + RC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + RC::TWQ;
+  xb_setup(xb, reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + RC::MB_OFF), line, LPC, RC::NT);
   // persistent: tiles of LPC rows, tile index fastest, then items (a.tiles per item)
   const int tiles = (int)a.tiles;
   const int total = tiles * (int)a.items;
@@ -1306,8 +1343,10 @@ __global__ void __launch_bounds__(RowCfg<LH>::NT, RowCfg<LH>::MINB) row_kernel(c
   auto put = [&](double* dst, int r, double x0, double x1) {
     const int n = 2 * LN::in_idx(t, r);
     if (!valid || n >= a.n_out || (EIK_DBG_ROW_NOST && a.n_comp < 100)) return;
-    if (even) *reinterpret_cast<double2*>(dst + obase + n) = make_double2(x0, x1);
-    else { dst[obase + n] = x0; if (n + 1 < a.n_out) dst[obase + n + 1] = x1; }
+    if (even) {
+      if constexpr (EIK_CS >= 2) __stcs(reinterpret_cast<double2*>(dst + obase + n), make_double2(x0, x1));
+      else *reinterpret_cast<double2*>(dst + obase + n) = make_double2(x0, x1);
+    } else { dst[obase + n] = x0; if (n + 1 < a.n_out) dst[obase + n + 1] = x1; }
   };
   auto putb = [&](uint8_t* dst, int r, uint8_t x0, uint8_t x1) {
     const int n = 2 * LN::in_idx(t, r);
