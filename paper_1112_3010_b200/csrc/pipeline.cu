@@ -2,6 +2,7 @@
 // spectra, workspaces), the pass schedule of the 2-D / 3-D pipelines, and the
 // extern "C" entry points declared in include/eikfld_b200.h.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
 
 #include <atomic>
 #include <climits>
@@ -541,6 +542,14 @@ struct Roles {
   int n_comp() const { return n_dist() + (sign ? 1 : 0); }
 };
 
+// NVTX range over a pass (visible in Nsight Systems / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // run_locked's profiling hook, visible to the pass functions (nullptr: not profiling)
 using MarkFn = std::function<int(int, bool)>;
 thread_local const MarkFn* g_mark = nullptr;
@@ -586,6 +595,7 @@ int set_components(const eik_plan* p, bool sign_group, const Roles& r, ColArgs& 
 // prepared by an earlier call with prep = true over the whole batch)
 int pass_col2d(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
                const Roles& r, double2* const* W, cudaStream_t st, int64_t b0 = 0, bool prep = true) {
+  NvtxRange nv(sg ? "eik:col2d(sign)" : "eik:col2d(distance)");
   DevBuf& rid = sg ? p->srowid : p->rowid;
   DevBuf& cl = sg ? p->scols : p->cols;
   DevBuf& rp = sg ? p->srowptr : p->rowptr;
@@ -679,6 +689,7 @@ struct PeerBlk {
 int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, int64_t K, int64_t B, const double* w,
                 int64_t c0loc, int64_t ks, double2* const* V, cudaStream_t st, const PeerBlk* pb = nullptr,
                 int in0 = 0, int nin = -1) {
+  NvtxRange nv(sg ? "eik:planes(sign)" : "eik:planes(distance)");
   const int64_t H = p->H, c1 = p->c[1], c2 = p->c[2];
   DevBuf& rid = sg ? p->srowid : p->rowid;
   DevBuf& cl = sg ? p->scols : p->cols;
@@ -757,6 +768,7 @@ int pass_planes(eik_plan* p, bool sg, const int64_t* nodes, const int64_t* off, 
 // V[i][i0 < c0][k1'][k2]; writes W_j[n < c0][k1'][k2].
 int pass_axis0(eik_plan* p, bool sg, double2* const* V, int64_t k1b, int64_t ks, int64_t B, const Roles& r,
                double2* const* W, cudaStream_t st, const PeerBlk* pb = nullptr) {
+  NvtxRange nv(sg ? "eik:axis0(sign)" : "eik:axis0(distance)");
   const int64_t H = p->H;
   if (k1b < p->k1_begin || k1b + ks > p->k1_begin + p->k1_count)
     return fail(EIK_EVALIDATION, "k1 slab not covered by the plan's kernel spectra");
@@ -799,6 +811,7 @@ struct RawOut {
 int pass_finish(eik_plan* p, double2* const* W, const Roles& r, int64_t c0loc, int64_t ks, int64_t B,
                 RowArgs ra, cudaStream_t st, const std::function<int(int, bool)>& mark,
                 const ChunkFn& on_chunk = nullptr, const RawOut* raw = nullptr) {
+  NvtxRange nv("eik:finish(lines+row)");
   const int64_t H = p->H;
   // raw: W[0..n) are written as scaled real-space convolutions (tau > 0: -tau log), no epilogue
   const int nc = raw ? raw->n : r.n_comp();
@@ -1097,6 +1110,7 @@ int eik_run(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t 
 }
 
 static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out, uint32_t flags, void* stream) {
+  NvtxRange nv("eik_run");
   p->run_gen = p->run_gen == INT_MAX ? 1 : p->run_gen + 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t B = in->batch < 1 ? 1 : in->batch;
