@@ -84,9 +84,16 @@ __host__ __device__ constexpr int col_pad(int L, bool pair) {
        : col_e(L) == 16 ? (L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT)
        : (L == 10) ? pad_code(3, 0, 3) : (L == 11) ? pad_code(2, 4, 6) : PAD_DEFAULT;
 }
+// threads per CTA of the TMEM column kernel of 2048-point lines: 256 = two lines per CTA, two
+// CTAs per SM (32-byte runs per row); 512 = four lines, one CTA per SM (64-byte runs)
+// (measured at 1024^3 with line-major spectra: 914 ms per step at 256, 789 ms at 512)
+#ifndef EIK_TM11_NT
+#define EIK_TM11_NT 512
+#endif
 __host__ __device__ constexpr int tm_pad(int L, bool pair) {
   return pair ? il2_pad(L, 16)
-       : L == 10 ? pad_code(2, 4, 0) : L == 11 ? pad_code(3, 5, 6) : L == 12 ? pad_code(4, 0, 0)
+       : L == 10 ? pad_code(2, 4, 0) : L == 11 ? (EIK_TM11_NT == 512 ? pad_code(3, 4, 0) : pad_code(3, 5, 6))
+       : L == 12 ? pad_code(4, 0, 0)
        : L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT;
 }
 __host__ __device__ constexpr int row_pad(int LH) {
@@ -111,6 +118,8 @@ struct ColCfg {
   using LN = PaddedLine<L, col_e(L), col_pad(L, IL == 2 && LPC > 2)>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
+  static constexpr int M0 = 1 << L;  // transform length the register-order spectrum copy indexes
+  __device__ static __forceinline__ int k0_of(int tid, int r) { return LN::out_idx(t_of(tid), r); }
   // ping-pong exchange buffers (one barrier per exchange instead of two) where
   // they were measured to pay off without costing occupancy (C5-sized lines)
   static constexpr int NBUF = ((L == 10 || L == 11) && (2 * LPC * LN::SMEM + LN::TWQ) * 16 <= 200 * 1024) ? 2 : 1;
@@ -180,6 +189,12 @@ struct KSpec {
   int imag;
   int odd0;
   int odd1;  // 3-D: odd along axis 1 (sign of the k1-mirrored lines, see ColArgs::fold_H)
+  // Line-major storage (3-D plans): ls > 0 means re[l * ls + k0] (one contiguous run of
+  // M0/2 + 1 values per spectral line, ls >= M0/2 + 1), so a column kernel's warp reads
+  // consecutive k0 of its lines as whole cache lines; ls == 0 is re[k0 * ld + l].  (At
+  // 1024^3 the k0-major layout cost 16 useful bytes per 64-byte DRAM burst: 249 GB read per
+  // axis-0 pass against 43 GB needed, profiles/round2/c4prof.)
+  int64_t ls;
   // Optional register-order copy (real/imaginary spectra, 2-D plans): the value
   // register r of thread tid of CTA tile b needs, at perm[(b * EPT + r) * NT + tid],
   // unfolded with the axis-0 parity sign applied.  Warp loads are contiguous
@@ -217,6 +232,7 @@ struct ColArgs {
   int spec_mode;
   double* spec_re[3];
   int64_t spec_ld;
+  int64_t spec_ls;  // > 0: line-major real / imaginary spectrum, spec_re[l * spec_ls + k0] (KSpec::ls)
   const double2* tw;
   int lmax;
   // persistent TMEM column kernels (set by the launcher): tiles of LPC lines per item, items
@@ -298,9 +314,11 @@ __device__ __forceinline__ int64_t fold_line(const ColArgs& a, int64_t l, bool& 
 
 // Raw folded kernel spectrum value at (k0, l); the fold sign is applied at use
 // time (kapply) so a prefetch issued one FFT ahead does not stall on the load.
+template <bool LM = false>
 __device__ __forceinline__ double kload(const KSpec& k, int64_t l, int k0, int M0) {
   const bool hi = k0 > (M0 >> 1);
-  return __ldg(k.re + (int64_t)(hi ? M0 - k0 : k0) * k.ld + l);
+  if constexpr (LM) return __ldg(k.re + l * k.ls + (hi ? M0 - k0 : k0));
+  else return __ldg(k.re + (int64_t)(hi ? M0 - k0 : k0) * k.ld + l);
 }
 // All EPT kernel-spectrum values of this thread for a kernel of configuration
 // CFG (one uniform branch on the layout, outside the unrolled loads).
@@ -318,10 +336,13 @@ __device__ __forceinline__ void perm_thread(int& tc, int& rev) {
     }
   }
 }
-template <class CFG>
+// LM: line-major storage (KSpec::ls), a compile-time property of the 3-D instantiations so
+// that the 2-D kernels' code is untouched (a run-time layout select in the unrolled loads
+// cost C3's column kernel 16% and C2's 3%)
+template <class CFG, bool LM = false>
 __device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpec& k, int64_t l, int t, int64_t bx) {
   using LN = typename CFG::LN;
-  if (k.perm) {
+  if (!LM && k.perm) {
     int tc, rev;
     perm_thread<CFG>(tc, rev);
     const double* __restrict__ src = k.perm + bx * LN::EPT * CFG::NTP + tc;
@@ -329,15 +350,27 @@ __device__ __forceinline__ void kload_all(double (&kn)[CFG::LN::EPT], const KSpe
     for (int r = 0; r < LN::EPT; ++r) kn[r] = __ldg(src + (rev ? LN::EPT - 1 - r : r) * CFG::NTP);
   } else {
 #pragma unroll
-    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload(k, l, LN::out_idx(t, r), LN::M);
+    for (int r = 0; r < LN::EPT; ++r) kn[r] = kload<LM>(k, l, LN::out_idx(t, r), LN::M);
   }
+}
+// Register-resident column kernel (the EIK_TMEM=0 fallback): the layout is a uniform run-time
+// branch, and only for the line lengths whose 3-D plans store line-major spectra.
+template <class CFG>
+__device__ __forceinline__ void kload_rt(double (&kn)[CFG::LN::EPT], const KSpec& k, int64_t l, int t, int64_t bx) {
+  if constexpr (CFG::LN::L >= 10) {
+    if (k.ls) {
+      kload_all<CFG, true>(kn, k, l, t, bx);
+      return;
+    }
+  }
+  kload_all<CFG, false>(kn, k, l, t, bx);
 }
 // L1 prefetch of this thread's EPT kernel-spectrum values (TMEM column kernel).
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-template <class CFG>
+template <class CFG, bool LM = false>
 __device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t, int64_t bx) {
   using LN = typename CFG::LN;
-  if (k.perm) {
+  if (!LM && k.perm) {
     int tc, rev;
     perm_thread<CFG>(tc, rev);
     const double* src = k.perm + bx * LN::EPT * CFG::NTP + tc;
@@ -348,7 +381,12 @@ __device__ __forceinline__ void kprefetch_all(const KSpec& k, int64_t l, int t, 
     for (int r = 0; r < LN::EPT; ++r) {
       const int k0 = LN::out_idx(t, r);
       const bool hi = k0 > (LN::M >> 1);
-      prefetch_l1(k.re + (int64_t)(hi ? LN::M - k0 : k0) * k.ld + l);
+      const int kf = hi ? LN::M - k0 : k0;
+      if constexpr (LM) {
+        if ((kf & 15) == 0) prefetch_l1(k.re + l * k.ls + kf);  // one request per 128-byte run
+      } else {
+        prefetch_l1(k.re + (int64_t)kf * k.ld + l);
+      }
     }
   }
 }
@@ -479,7 +517,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
     const int64_t lk = fold_line(a, l, mir);
     double kn[LN::EPT];  // next component's kernel spectrum, prefetched
     if (real_ks && valid) {
-      kload_all<ColCfg<L>>(kn, a.ks[0], lk, t, blockIdx.x);
+      kload_rt<ColCfg<L>>(kn, a.ks[0], lk, t, blockIdx.x);
     }
 #pragma unroll 1
     for (int j = 0; j < a.n_comp; ++j) {
@@ -489,7 +527,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
         for (int r = 0; r < LN::EPT; ++r)
           y[r] = valid ? kapply(v[r], kn[r], a.ks[j], LN::out_idx(t, r), LN::M, mir) : v[r];
         if (j + 1 < a.n_comp && valid) {
-          kload_all<ColCfg<L>>(kn, a.ks[j + 1], lk, t, blockIdx.x);
+          kload_rt<ColCfg<L>>(kn, a.ks[j + 1], lk, t, blockIdx.x);
         }
       } else {
 #pragma unroll
@@ -518,7 +556,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
       const int64_t lk = fold_line(a, l, mir);
       double kn[LN::EPT];  // this input's kernel spectrum, loaded before its transform
       if (real_ks && valid) {
-        kload_all<ColCfg<L>>(kn, a.ks[i], lk, t, blockIdx.x);
+        kload_rt<ColCfg<L>>(kn, a.ks[i], lk, t, blockIdx.x);
       }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, i, valid);
@@ -553,7 +591,9 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) col_kernel(const __grid_constan
         } else if (a.spec_mode == SPEC_COMPLEX_T) {
           a.out[i][(int64_t)k0 * a.spec_ld + l] = v[r];
         } else if (k0 <= (LN::M >> 1)) {
-          a.spec_re[i][(int64_t)k0 * a.spec_ld + l] = (a.spec_mode == SPEC_REAL_T) ? v[r].x : v[r].y;
+          const double part = (a.spec_mode == SPEC_REAL_T) ? v[r].x : v[r].y;
+          if (a.spec_ls) a.spec_re[i][l * a.spec_ls + k0] = part;
+          else a.spec_re[i][(int64_t)k0 * a.spec_ld + l] = part;
         }
       }
     }
@@ -612,7 +652,8 @@ struct TmCfg {
   static constexpr int E = (EIK_TM_E == 8 && L >= EIK_TM_E8_MINL && L <= EIK_TM_E8_MAXL) ? 8 : 16;
   static constexpr int TPL0 = tpl_of(L, E);
   static constexpr bool F4K = (L == 12 && EIK_FOUR_STEP && E == 16);
-  static constexpr int NT = F4K ? 256 * LPCX : E == 8 ? (L >= 12 ? 1024 : 512) : (TPL0 > 256 ? TPL0 : 256);
+  static constexpr int NT = F4K ? 256 * LPCX : E == 8 ? (L >= 12 ? 1024 : 512)
+                            : (L == 11 && E == 16) ? EIK_TM11_NT : (TPL0 > 256 ? TPL0 : 256);
   static constexpr int LPC = NT / TPL0;
   static constexpr int MINB = E == 8 ? (NT >= 1024 ? 1 : 2) : (NT >= 512 ? 1 : 2);
   // four-step lines: EIK_F4K_IL = 1 makes the CTA line-major (warps 0-7 line 0,
@@ -625,6 +666,8 @@ struct TmCfg {
   using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
+  static constexpr int M0 = 1 << L;
+  __device__ static __forceinline__ int k0_of(int tid, int r) { return LN::out_idx(t_of(tid), r); }
   // Folded register-order kernel spectra (four-step lines, two lanes-interleaved
   // lines): thread t = 16 a + b holds k0 = a + 16 b + 256 r, whose mirror
   // M - k0 is held by thread 16 (16 - a) + 15 - b at register 15 - r.  Warps
@@ -697,7 +740,7 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 #ifndef EIK_DBG_STAGEONLY
 #define EIK_DBG_STAGEONLY 0
 #endif
-template <int L, int IN, int OUT, bool HALF>
+template <int L, int IN, int OUT, bool HALF, bool LM = false>
 __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpcx(L, OUT)>::MINB)
     col_tmem_kernel(const __grid_constant__ ColArgs a) {
   using TC = TmCfg<L, tm_lpcx(L, OUT)>;
@@ -769,7 +812,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       // y = sum_i K_i X_i accumulated in TMEM while each input is transformed in registers
 #pragma unroll 1
       for (int i = 0; i < a.n_in; ++i) {
-        if (valid) kprefetch_all<TC>(a.ks[i], lk, t, bx);  // into L1 while the input is transformed
+        if (valid) kprefetch_all<TC, LM>(a.ks[i], lk, t, bx);  // into L1 while the input is transformed
         if constexpr (IN == IN_SPARSE) {
           load_sparse<LN, HALF>(v, a, t, l, item, i, valid, twq);
         } else {
@@ -781,7 +824,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
         fft_line<LN, false, HALF>(v, t, xb, tws);
         double kn[LN::EPT];
         if (valid) {
-          kload_all<TC>(kn, a.ks[i], lk, t, bx);
+          kload_all<TC, LM>(kn, a.ks[i], lk, t, bx);
           kapply_all<LN>(v, kn, a.ks[i], t, mir);
         } else {
 #pragma unroll
@@ -827,14 +870,14 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
         else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
         fft_line<LN, false, HALF>(v, t, xb, tws, hook);
         tmem_put(ta, v);
-        if (valid) kprefetch_all<TC>(a.ks[0], lk, t, bx);
+        if (valid) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
 #pragma unroll 1
         for (int j = 0; j < a.n_comp; ++j) {
           tmem_get(ta, v);
           if (valid) {
             double kn[LN::EPT];
-            kload_all<TC>(kn, a.ks[j], lk, t, bx);
-            if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], lk, t, bx);
+            kload_all<TC, LM>(kn, a.ks[j], lk, t, bx);
+            if (j + 1 < a.n_comp) kprefetch_all<TC, LM>(a.ks[j + 1], lk, t, bx);
             kapply_all<LN>(v, kn, a.ks[j], t, mir);
           }
           fft_line<LN, true>(v, t, xb, tws, hook);
@@ -868,15 +911,15 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
       tmem_put(ta, v);
       // kernel spectra: the next component's lines are prefetched into L1 one
       // transform ahead (no registers held across the FFT); loaded at use
-      if (valid && !EIK_DBG_NOK) kprefetch_all<TC>(a.ks[0], lk, t, bx);
+      if (valid && !EIK_DBG_NOK) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
       next_prefetch();
 #pragma unroll 1
       for (int j = 0; j < a.n_comp; ++j) {
         tmem_get(ta, v);
         if (valid && !EIK_DBG_NOK) {
           double kn[LN::EPT];
-          kload_all<TC>(kn, a.ks[j], lk, t, bx);
-          if (j + 1 < a.n_comp) kprefetch_all<TC>(a.ks[j + 1], lk, t, bx);
+          kload_all<TC, LM>(kn, a.ks[j], lk, t, bx);
+          if (j + 1 < a.n_comp) kprefetch_all<TC, LM>(a.ks[j + 1], lk, t, bx);
           kapply_all<LN>(v, kn, a.ks[j], t, mir);
         }
         fft_line<LN, true>(v, t, xb, tws);
@@ -931,6 +974,219 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpc
   tmem_free_cta(tbase, TC::COLS);
 }
 
+// ---------------------------------------------------------------------------
+// Even / odd split column kernel for 4096-point lines (distance group).
+//
+// A half-padded 4096-point forward transform is two independent 2048-point
+// transforms of the same input: X[2k] = FFT2048(x)[k], X[2k+1] = FFT2048(x W4096^n)[k],
+// and the first 2048 outputs of the inverse are
+//   y[n] = IFFT2048(Y_even)[n] + conj(W4096^n) IFFT2048(Y_odd)[n].
+// The 512-thread CTA is two groups of 8 warps: group 0 owns the even bins of
+// the tile's two lines, group 1 the odd bins.  Each group runs the 2048-point
+// Stockham schedule (lines interleaved by lane parity, like the 256-thread TMEM
+// kernel of 2048-point lines) on its own exchange buffers under its own named
+// barrier, keeps its half of the forward spectrum in TMEM, and multiplies its
+// half of every kernel spectrum.  Per component group 1 hands its twiddled
+// result to group 0 through a shared-memory buffer, warp to warp (thread
+// (line, t) of both groups holds the same n): one mbarrier pair per warp pair,
+// no CTA-wide barrier anywhere.  Group 0 adds and stores.  The groups therefore
+// run out of phase (group 1 one hand-over ahead): one group's FP64 butterflies
+// overlap the other's shared-memory exchange and global stores, which the
+// lock-step 16-warp kernel cannot do.
+// Measured on the B200 (C2, tools/gpu_eo1.sh, profiles/round2/eo/): parity green, but the
+// column kernel takes 0.415 ms against 0.318 ms for the 16-warp four-step kernel, and its
+// parts are additive as well (no FP64 -82 us, no exchanges -104, no stores -63, no hand-over
+// -28, no spectrum loads -28): eight warps per group do not fill a unit within a phase, so
+// the out-of-phase groups hide nothing.  Off by default (-DEIK_EO=1 builds it, EIK_EO=0 at
+// run time then selects the four-step kernel).
+#ifndef EIK_EO
+#define EIK_EO 0
+#endif
+#ifndef EIK_DBG_NOHAND
+#define EIK_DBG_NOHAND 0  // timing probe: no hand-over between the groups (wrong results)
+#endif
+struct LineEO : PaddedLine<11, 16, pad_code(3, 5, 6)> {
+  // only the inverse's NS = 16 stage keeps a stage table (240 entries); every
+  // other twiddle comes from the quarter table or this thread's TMEM constants
+  static constexpr bool INV_SHARES = false;
+  __host__ __device__ static constexpr bool st_quarter(bool inv, int s) { return s >= 1 && !(inv && s == 1); }
+  __host__ __device__ static constexpr int st_size(bool inv, int s) { return (inv && s == 1) ? 16 * 15 : 0; }
+  __host__ __device__ static constexpr int st_off(bool, int) { return 0; }
+  static constexpr int ST_SIZE = 16 * 15;
+};
+struct EoCfg {
+  using LN = LineEO;
+  static constexpr int NT = 512, GT = 256, LPC = 2, NTP = 512, M0 = 4096;
+  static constexpr bool PFOLD = false;
+  using XB = XBuf<1, 2, GT>;
+  __device__ static __forceinline__ int group_of(int tid) { return tid >> 8; }
+  __device__ static __forceinline__ int line_of(int tid) { return tid & 1; }
+  __device__ static __forceinline__ int t_of(int tid) { return (tid & 255) >> 1; }
+  __device__ static __forceinline__ int k0_of(int tid, int r) { return 2 * LN::out_idx(t_of(tid), r) + group_of(tid); }
+  static constexpr int WPT = 64, WPT_ALL = 128, COLS = 512;  // TMEM words per thread: spectrum half + constants
+  static constexpr size_t HB_OFF = (size_t)4 * LN::SMEM * sizeof(double2);
+  static constexpr size_t TWQ_OFF = HB_OFF + (size_t)16 * GT * sizeof(double2);
+  static constexpr size_t ST_OFF = TWQ_OFF + (size_t)LN::TWQ * sizeof(double2);
+  static constexpr size_t SLOT_OFF = ST_OFF + (size_t)LN::ST_SIZE * sizeof(double2);
+  static constexpr size_t MB_OFF = SLOT_OFF + 16;  // 2 exchange + 8 full + 8 empty mbarriers
+  static constexpr size_t SMEM_BYTES = MB_OFF + 18 * sizeof(uint64_t);
+};
+static_assert(EoCfg::SMEM_BYTES <= 227 * 1024, "even/odd column kernel: shared memory");
+
+// v[i] *= c[i] (or conj), the 16 per-thread constants at TMEM address a, four at a time
+template <bool CONJ>
+__device__ __forceinline__ void tmem_cmul16(uint32_t a, double2 (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t w32[16];
+    tmem_ld16(a + 16 * c, w32);
+    tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 w = make_double2(
+          __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 1] << 32) | w32[4 * q])),
+          __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 3] << 32) | w32[4 * q + 2])));
+      v[4 * c + q] = CONJ ? cmulc(v[4 * c + q], w) : cmul(v[4 * c + q], w);
+    }
+  }
+}
+
+template <int IN>
+__global__ void __launch_bounds__(EoCfg::NT, 1) col_eo_kernel(const __grid_constant__ ColArgs a) {
+  using TC = EoCfg;
+  using LN = LineEO;
+  extern __shared__ double2 smem[];
+  char* sbase = reinterpret_cast<char*>(smem);
+  const int tid = threadIdx.x;
+  const int g = TC::group_of(tid), line = TC::line_of(tid), t = TC::t_of(tid), tig = tid & (TC::GT - 1);
+  const int wp = tig >> 5;  // warp pair of the hand-over
+  typename TC::XB xb{smem + (g * 2 + line) * LN::SMEM, nullptr, 0, 1 + g};
+  double2* hb = reinterpret_cast<double2*>(sbase + TC::HB_OFF) + tig;  // [register][thread of the group]
+  double2* twq = reinterpret_cast<double2*>(sbase + TC::TWQ_OFF);
+  double2* sts = reinterpret_cast<double2*>(sbase + TC::ST_OFF);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(sbase + TC::SLOT_OFF);
+  uint64_t* mbs = reinterpret_cast<uint64_t*>(sbase + TC::MB_OFF);
+  uint64_t* mb_full = mbs + 2 + wp;
+  uint64_t* mb_empty = mbs + 10 + wp;
+  if (tid < 16) mbar_init(mbs + 2 + tid, 1u);
+  xb_setup(xb, mbs, g, 2, TC::NT);
+  twq_fill(twq, LN::L, a.tw, a.lmax);
+  st_fill<LN>(sts, a.tw, a.lmax);
+  const uint32_t tbase = tmem_alloc_cta(slot, TC::COLS);  // also publishes the tables and the mbarriers
+  const uint32_t ta = tmem_thread_addr(tbase, TC::WPT_ALL);
+  const uint32_t tc = ta + TC::WPT;
+  if (g) {  // W4096^n of this thread's 16 elements
+    double2 w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = __ldg(a.tw + ((int64_t)LN::in_idx(t, i) << (a.lmax - 12)));
+    tmem_put(tc, w);
+  } else {  // the last inverse stage's twiddles
+    tw_last_inv_fill<LN>(tc, t, twq, LN::L);
+  }
+  const TwSrc tws{sts, twq, LN::L, 0u, g ? 0u : tc};
+  const int tiles = (int)a.tiles;
+  const int total = tiles * (int)a.items;
+  uint32_t seq = 0;  // hand-overs so far (parity of the mbarrier phases)
+
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int item = tile / tiles;
+    const int bx = tile - item * tiles;
+    const int64_t l = (int64_t)bx * TC::LPC + line;
+    const bool valid = l < a.nlines;
+    bool mir;
+    const int64_t lk = fold_line(a, l, mir);
+    double2 v[16];
+    if constexpr (IN == IN_SPARSE) load_sparse<LN, false>(v, a, t, l, item, 0, valid, twq);
+    else load_dense<LN, false>(v, a, t, l, item, 0, valid);
+    if (g) tmem_cmul16<false>(tc, v);
+    fft_line<LN, false, false>(v, t, xb, tws);
+    tmem_put(ta, v);
+    auto kprefetch = [&](const KSpec& k) {  // the next component's values head for L2 (no L1 left next to 226 KB)
+      if (!valid) return;
+      if (k.perm) {
+        const double* src = k.perm + (int64_t)bx * 16 * TC::NTP + tid;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r * TC::NTP));
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int k0 = TC::k0_of(tid, r);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(k.re + (int64_t)(k0 > 2048 ? 4096 - k0 : k0) * k.ld + lk));
+        }
+      }
+    };
+    if (!EIK_DBG_NOK) kprefetch(a.ks[0]);
+#pragma unroll 1
+    for (int j = 0; j < a.n_comp; ++j) {
+      tmem_get(ta, v);
+      if (valid && !EIK_DBG_NOK) {
+        const KSpec& k = a.ks[j];
+        double kn[16];
+        if (k.perm) {
+          const double* __restrict__ src = k.perm + (int64_t)bx * 16 * TC::NTP + tid;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) kn[r] = __ldg(src + r * TC::NTP);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) kn[r] = kload(k, lk, TC::k0_of(tid, r), 4096);
+        }
+        if (j + 1 < a.n_comp) kprefetch(a.ks[j + 1]);
+        const bool neg1 = k.odd1 && mir;
+        if (k.odd0 || neg1) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if ((k.odd0 && TC::k0_of(tid, r) > 2048) != neg1) kn[r] = -kn[r];
+        }
+        if (k.imag) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) v[r] = make_double2(-v[r].y * kn[r], v[r].x * kn[r]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) v[r] = make_double2(v[r].x * kn[r], v[r].y * kn[r]);
+        }
+      }
+      fft_line<LN, true>(v, t, xb, tws);
+      if (g) {
+        tmem_cmul16<true>(tc, v);
+#if !EIK_DBG_NOHAND
+        mbar_wait(mb_empty, (seq & 1u) ^ 1u);  // group 0 has taken the previous hand-over
+#pragma unroll
+        for (int i = 0; i < 16; ++i) hb[i * TC::GT] = v[i];
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(mb_full);
+#endif
+      } else {
+#if !EIK_DBG_NOHAND
+        mbar_wait(mb_full, seq & 1u);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = cadd(v[i], hb[i * TC::GT]);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(mb_empty);
+#endif
+        if (a.accum) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = LN::in_idx(t, i);
+            if (valid && n < a.n_out) {
+              double2* dst = comp_dst(a, j, item, l, n);
+              *dst = cadd(*dst, v[i]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = LN::in_idx(t, i);
+            if (valid && n < a.n_out && !(EIK_DBG_NOST && a.n_comp < 100)) store_u(comp_dst(a, j, item, l, n), v[i]);
+          }
+        }
+      }
+      ++seq;
+    }
+  }
+  tmem_free_cta(tbase, TC::COLS);
+}
+
 // Register-order copy of a folded real/imaginary spectrum for the column
 // kernel configuration CFG (see KSpec::perm).  One thread per output value.
 template <class CFG>
@@ -943,11 +1199,11 @@ __global__ void spectrum_perm_kernel(const double* __restrict__ re, int64_t ld, 
     const int r = (int)(rest % LN::EPT);
     const int64_t b = rest / LN::EPT;
     const int64_t l = b * CFG::LPC + CFG::line_of(tid);
-    const int k0 = LN::out_idx(CFG::t_of(tid), r);
-    const bool hi = k0 > (LN::M >> 1);
+    const int k0 = CFG::k0_of(tid, r);
+    const bool hi = k0 > (CFG::M0 >> 1);
     double v = 0.0;
     if (l < nlines) {
-      v = re[(int64_t)(hi ? LN::M - k0 : k0) * ld + l];
+      v = re[(int64_t)(hi ? CFG::M0 - k0 : k0) * ld + l];
       if (odd0 && hi && !CFG::PFOLD) v = -v;  // folded copies: sign applied at use
     }
     kp[i] = v;

@@ -89,10 +89,19 @@ inline int persist_mode() {
 
 // Persistent launch of the TMEM column kernel: one resident wave of CTAs walks
 // the (item, tile) list (EIK_PERSIST=0: one CTA per tile, for A/B runs).
+// line-major kernel spectra (KSpec::ls, 3-D plans with an axis 0 of 1024 points and more) are a
+// compile-time property of the kernel: these are the instantiations that exist
+template <int L, int IN, int OUT>
+constexpr bool tmem_has_lm() { return L >= 10 && L <= 12 && IN == IN_DENSE && (OUT == OUT_COMPS || OUT == OUT_SUM); }
+
 template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_persistent(const ColArgs& a, int64_t items, cudaStream_t st) {
   using C = TmCfg<L, tm_lpcx(L, OUT)>;
-  auto k = col_tmem_kernel<L, IN, OUT, HALF>;
+  auto k = col_tmem_kernel<L, IN, OUT, HALF, false>;
+  if (a.ks[0].ls) {
+    if constexpr (tmem_has_lm<L, IN, OUT>()) k = col_tmem_kernel<L, IN, OUT, HALF, true>;
+    else return fail(EIK_EVALIDATION, "line-major kernel spectra: no column kernel for this shape");
+  }
   const size_t smem_max = C::SMEM_BYTES + ((EIK_DBG_STAGEONLY || C::TSTORE) && L == 12 ? 256 + (size_t)(C::LN::M / 2) * C::LPC * 16 : 0);
   CK(prep_kernel_attr(k, smem_max));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
@@ -128,6 +137,41 @@ int launch_tmem_persistent(const ColArgs& a, int64_t items, cudaStream_t st) {
   k<<<(unsigned)grid, C::NT, smem_bytes, st>>>(b);
   CK(cudaGetLastError());
   return EIK_OK;
+}
+
+// Even / odd split kernel for the distance group's 4096-point lines (col_eo_kernel);
+// EIK_EO=0 at run time keeps the 16-warp four-step kernel (the register-order
+// spectrum copies follow the same switch, so it is read once per process)
+inline bool use_eo() {
+  static const bool on = [] {
+    const char* e = std::getenv("EIK_EO");
+    return EIK_EO && !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <int IN>
+int launch_eo(const ColArgs& a, int64_t items, cudaStream_t st) {
+  if constexpr (EIK_EO) {
+  using C = EoCfg;
+  auto k = col_eo_kernel<IN>;
+  CK(prep_kernel_attr(k, C::SMEM_BYTES));
+  const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
+  if (tiles <= 0 || items <= 0) return EIK_OK;
+  const int64_t total = tiles * items;
+  if (total > 0x7fffffffLL) return fail(EIK_EVALIDATION, "too many column tiles in one launch");
+  ColArgs b = a;
+  b.tiles = tiles;
+  b.items = items;
+  b.tstore = 0;
+  const int pm = persist_mode();
+  const int64_t wave = sm_count();
+  const int64_t grid = pm == 0 ? total : (total < wave ? total : wave);
+  k<<<(unsigned)grid, C::NT, C::SMEM_BYTES, st>>>(b);
+  CK(cudaGetLastError());
+  return EIK_OK;
+  } else {
+    return fail(EIK_EVALIDATION, "even/odd column kernel not built (-DEIK_EO=1)");
+  }
 }
 
 template <int IN, int OUT, bool HALF>

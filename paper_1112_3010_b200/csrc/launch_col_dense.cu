@@ -19,6 +19,10 @@ int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
+  if constexpr (EIK_EO && L == 12 && OUT == OUT_COMPS && HALF) {
+    if (use_tmem() && use_eo() && a.ks[0].cplx == nullptr && !a.ks[0].ls && a.n_valid <= 2048 && a.n_out <= 2048)
+      return launch_eo<IN>(a, items, st);
+  }
   if constexpr ((OUT == OUT_COMPS || OUT == OUT_SUM) && L >= 9) {
     if (use_tmem() && a.ks[0].cplx == nullptr) return launch_tmem_t<L, IN, OUT, HALF>(a, items, st);
   }
@@ -53,6 +57,9 @@ int permute_t(const double* re, int64_t ld, int64_t nlines, int odd0, double* kp
 int launch_spectrum_perm(int L, bool sum, const double* re, int64_t ld, int64_t nlines, int odd0, double* kp,
                          int64_t* elems, int* folded, cudaStream_t st) {
 #define EIK_PERM(Lc)                                                                                     \
+  if constexpr (EIK_EO && Lc == 12) {                                                                    \
+    if (use_tmem() && use_eo() && !sum) return permute_t<EoCfg>(re, ld, nlines, odd0, kp, elems, folded, st);  \
+  }                                                                                                      \
   if constexpr (Lc >= 9) {                                                                               \
     if (use_tmem())                                                                                      \
       return sum ? permute_t<TmCfg<Lc, tm_lpcx(Lc, OUT_SUM)>>(re, ld, nlines, odd0, kp, elems, folded, st)       \

@@ -18,6 +18,10 @@ int launch_tmem_t(const ColArgs& a, int64_t items, cudaStream_t st) {
 
 template <int L, int IN, int OUT, bool HALF>
 int launch_col_t(const ColArgs& a, int64_t items, cudaStream_t st) {
+  if constexpr (EIK_EO && L == 12 && OUT == OUT_COMPS && HALF) {
+    if (use_tmem() && use_eo() && a.ks[0].cplx == nullptr && !a.ks[0].ls && a.n_valid <= 2048 && a.n_out <= 2048)
+      return launch_eo<IN>(a, items, st);
+  }
   if constexpr ((OUT == OUT_COMPS || OUT == OUT_SUM) && L >= 9) {
     if (use_tmem() && a.ks[0].cplx == nullptr) return launch_tmem_t<L, IN, OUT, HALF>(a, items, st);
   }
