@@ -179,6 +179,24 @@ def algorithmic_bytes(plan_info, w, batch):
     return out
 
 
+def c4_step_bytes(counts, padded):
+    """Compulsory HBM bytes of one fused C4 step (S + grad S + degree sign), 3-D pass model of
+    algorithmic_bytes_3d extended by the sign group: three flux inputs (T and V round trips,
+    one folded spectrum each), one summed component through the lines and row passes, mu and
+    the mask.  The streamed one-GPU schedule moves more (it repeats the axis-0 forward per
+    component and accumulates the sign component in HBM); this is the bound, not its traffic."""
+    c0, c1, c2 = counts
+    M0, M1, M2 = padded[:3]
+    H = M2 // 2 + 1
+    ks = (M0 // 2 + 1) * (M1 // 2 + 1) * H * 8
+    plane = 16 * c0 * M1 * H
+    slab = 16 * c0 * c1 * H
+    N = c0 * c1 * c2
+    dist = (2 * slab + 2 * plane) + 4 * (ks + 2 * plane + 2 * slab + 8 * N)
+    sign = 3 * (2 * slab + 2 * plane + ks) + (2 * plane + 2 * slab) + 9 * N
+    return dist + sign
+
+
 def algorithmic_bytes_3d(plan_info, w, batch):
     """3-D pass model (c0 x c1 x c2 grid, M = 2c, H = M2/2+1).
 
@@ -756,6 +774,18 @@ def bench_c4_single(a):
              profile=True)  # untimed: per-pass device times
     torch.cuda.synchronize()
     pt = plan.pass_times()
+    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback"
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
+    step_s = total_ms / a.steps / 1e3
+    sb = c4_step_bytes(grid.counts, info["padded"])
+    roof = {"bound": "hbm", "achieved": round(sb / step_s / 1e9, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(sb / step_s / 1e9 / peak, 4), "traffic": None,
+            "kernel": "whole step (chain of axis passes; fused-schedule pass model)", "algorithmic_bytes": sb,
+            "peak_source": peak_src,
+            "survey_pass_model": {"bytes_per_point": SURVEY_BYTES_PER_POINT["C4"], "step_bytes": SURVEY_BYTES_PER_POINT["C4"] * N,
+                                  "step_frac": round(SURVEY_BYTES_PER_POINT["C4"] * N / step_s / 1e9 / peak, 4)}}
     line = {
         "metric": "grid points/sec (S+grad S+sign)", "value": value, "unit": "grid_points/s", "n_gpus": 1,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
@@ -769,7 +799,7 @@ def bench_c4_single(a):
                    "device_total_bytes": int(tot_b), "inside_fraction": round(inside, 6)},
         "e2e": e2e,
         "gpu_launches": None,
-        "roofline": None,
+        "roofline": roof,
         "pass_ms": pt,
         "cpu_baseline": {"value": None, "unit": "grid_points/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": "infeasible: the reference pads to 3072^3 (464 GB per complex array) and "

@@ -86,13 +86,17 @@ __host__ __device__ constexpr int col_pad(int L, bool pair) {
 }
 // threads per CTA of the TMEM column kernel of 2048-point lines: 256 = two lines per CTA, two
 // CTAs per SM (32-byte runs per row); 512 = four lines, one CTA per SM (64-byte runs)
-// (measured at 1024^3 with line-major spectra: 914 ms per step at 256, 789 ms at 512)
+// (measured at 1024^3 with line-major spectra: 914 ms per step at 256, 789 ms at 512).  The
+// 3-D instantiations (TmCfg<.., WIDE = true>, selected with the line-major spectra) always run
+// 512 threads for 1024- and 2048-point lines: 8 / 4 lines per CTA, 128- / 64-byte runs per row
+// of arrays whose rows lie tens of MB apart; the 2-D kernels keep two 256-thread CTAs per SM.
 #ifndef EIK_TM11_NT
-#define EIK_TM11_NT 512
+#define EIK_TM11_NT 256
 #endif
-__host__ __device__ constexpr int tm_pad(int L, bool pair) {
+__host__ __device__ constexpr int tm_pad(int L, bool pair, bool wide = false) {
   return pair ? il2_pad(L, 16)
-       : L == 10 ? pad_code(2, 4, 0) : L == 11 ? (EIK_TM11_NT == 512 ? pad_code(3, 4, 0) : pad_code(3, 5, 6))
+       : L == 10 ? (wide ? pad_code(2, 0, 0) : pad_code(2, 4, 0))
+       : L == 11 ? ((wide || EIK_TM11_NT == 512) ? pad_code(3, 4, 0) : pad_code(3, 5, 6))
        : L == 12 ? pad_code(4, 0, 0)
        : L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT;
 }
@@ -647,12 +651,13 @@ __host__ __device__ constexpr int tm_lpcx(int L, int OUT) {
 #ifndef EIK_TM_E8_MINL
 #define EIK_TM_E8_MINL 10
 #endif
-template <int L, int LPCX = 1>
+template <int L, int LPCX = 1, bool WIDE = false>
 struct TmCfg {
   static constexpr int E = (EIK_TM_E == 8 && L >= EIK_TM_E8_MINL && L <= EIK_TM_E8_MAXL) ? 8 : 16;
   static constexpr int TPL0 = tpl_of(L, E);
   static constexpr bool F4K = (L == 12 && EIK_FOUR_STEP && E == 16);
   static constexpr int NT = F4K ? 256 * LPCX : E == 8 ? (L >= 12 ? 1024 : 512)
+                            : (WIDE && E == 16 && (L == 10 || L == 11)) ? 512
                             : (L == 11 && E == 16) ? EIK_TM11_NT : (TPL0 > 256 ? TPL0 : 256);
   static constexpr int LPC = NT / TPL0;
   static constexpr int MINB = E == 8 ? (NT >= 1024 ? 1 : 2) : (NT >= 512 ? 1 : 2);
@@ -662,7 +667,7 @@ struct TmCfg {
   static constexpr int IL = F4K ? (EIK_F4K_IL < LPC ? EIK_F4K_IL : LPC) : col_il(LPC);
   using LN = std::conditional_t<F4K, Line4K,
                                 std::conditional_t<E == 8, PaddedLine<L, 8, col_pad(L, IL == 2 && LPC > 2)>,
-                                                   PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2)>>>;
+                                                   PaddedLine<L, 16, tm_pad(L, IL == 2 && LPC > 2, WIDE)>>>;
   using XB = XBuf<1, group_sync(IL, LPC, TPL0), IL * TPL0>;
   __device__ static __forceinline__ int line_of(int tid) { return (tid / (IL * TPL0)) * IL + tid % IL; }
   __device__ static __forceinline__ int t_of(int tid) { return (tid % (IL * TPL0)) / IL; }
@@ -741,9 +746,9 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 #define EIK_DBG_STAGEONLY 0
 #endif
 template <int L, int IN, int OUT, bool HALF, bool LM = false>
-__global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT)>::NT, TmCfg<L, tm_lpcx(L, OUT)>::MINB)
+__global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT), LM>::NT, TmCfg<L, tm_lpcx(L, OUT), LM>::MINB)
     col_tmem_kernel(const __grid_constant__ ColArgs a) {
-  using TC = TmCfg<L, tm_lpcx(L, OUT)>;
+  using TC = TmCfg<L, tm_lpcx(L, OUT), LM>;
   using LN = typename TC::LN;
   constexpr int LPC = TC::LPC;
   extern __shared__ double2 smem[];
@@ -1227,19 +1232,48 @@ struct LinesArgs {
   // blk[n >> split_shift_out] + c * blk_cstride + o * outer_out + q + (n mod 2^shift) * es_out
   double2* blk[MAXG];
   int64_t blk_cstride;
+  // set by the launcher: tiles of LPC lines per component, components
+  int64_t tiles;
+  int ncomp;
 };
 
+// Lines of 1024 to 4096 points: 16 values per thread (two exchanges instead of the three of the
+// radix-8 column configuration, which needs its registers for the product as well), 512 threads,
+// i.e. 8 / 4 / 2 adjacent lines per CTA (128- / 64- / 32-byte runs per element), persistent CTAs
+// (tables filled once per SM instead of once per 2 lines).  EIK_LINES_E16=0: the column configuration.
+#ifndef EIK_LINES_E16
+#define EIK_LINES_E16 1
+#endif
+template <int L>
+struct LinesCfg16 {
+  static constexpr int TPL0 = (1 << L) / 16;
+  static constexpr int NT = 512;
+  static constexpr int LPC = NT / TPL0;
+  static constexpr int IL = LPC;
+  static constexpr bool PERSIST = true;
+  using LN = PaddedLine<L, 16, (L == 10 ? pad_code(2, 0, 0) : L == 11 ? pad_code(3, 4, 0) : pad_code(4, 0, 5))>;
+  __device__ static __forceinline__ int line_of(int tid) { return tid % LPC; }
+  __device__ static __forceinline__ int t_of(int tid) { return tid / LPC; }
+  static constexpr int NBUF = 1;
+  using XB = XBuf<1, 0, NT, false>;
+  static constexpr size_t MB_OFF = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
+  static constexpr size_t SMEM_BYTES = MB_OFF + 128;
+};
+template <int L>
+struct LinesColCfg : ColCfg<L> {
+  static constexpr bool PERSIST = false;
+};
+template <int L>
+using LinesCfg = std::conditional_t<(EIK_LINES_E16 && L >= 10 && L <= 12), LinesCfg16<L>, LinesColCfg<L>>;
+
 template <int L, bool INV, bool HALF>
-__global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_constant__ LinesArgs a) {
-  using LN = typename ColCfg<L>::LN;
-  constexpr int LPC = ColCfg<L>::LPC;
+__global__ void __launch_bounds__(LinesCfg<L>::NT) lines_kernel(const __grid_constant__ LinesArgs a) {
+  using CC = LinesCfg<L>;
+  using LN = typename CC::LN;
+  constexpr int LPC = CC::LPC;
   extern __shared__ double2 smem[];
-  const int line = ColCfg<L>::line_of(threadIdx.x);
-  const int t = ColCfg<L>::t_of(threadIdx.x);
-  const int64_t l = (int64_t)blockIdx.x * LPC + line;
-  const bool valid = l < a.nlines;
-  const int c = blockIdx.y;
-  using CC = ColCfg<L>;
+  const int line = CC::line_of(threadIdx.x);
+  const int t = CC::t_of(threadIdx.x);
   typename CC::XB xb{smem + line * LN::SMEM, smem + (LPC + line) * LN::SMEM, 0, 1 + line / CC::IL};
   double2* twq = smem + CC::NBUF * LPC * LN::SMEM;
   double2* sts = twq + LN::TWQ;
@@ -1249,6 +1283,13 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
   st_fill<LN>(sts, a.tw, a.lmax);
   __syncthreads();
   const TwSrc tws{sts, twq, L, 0u};
+  // (component, tile) work items, tile fastest; one per CTA unless the launch is persistent
+  const int64_t total = a.tiles * a.ncomp;
+#pragma unroll 1
+  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+  const int c = (int)(w / a.tiles);
+  const int64_t l = (w - c * a.tiles) * LPC + line;
+  const bool valid = l < a.nlines;
   const int64_t o = valid ? l / a.inner : 0, q = valid ? l % a.inner : 0;
   const double2* src = a.in[c] + o * a.outer_in + q;
   double2* dst = a.out[c] + o * a.outer_out + q;
@@ -1262,7 +1303,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
                : make_double2(0.0, 0.0);
   }
   fft_line<LN, INV, HALF>(v, t, xb, tws);
-  if (!valid) return;
+  if (!valid) continue;
 #pragma unroll
   for (int r = 0; r < LN::EPT; ++r) {
     const int n = INV ? LN::in_idx(t, r) : LN::out_idx(t, r);
@@ -1273,6 +1314,7 @@ __global__ void __launch_bounds__(ColCfg<L>::NT) lines_kernel(const __grid_const
       if (a.blk[0]) a.blk[n >> a.split_shift_out][c * a.blk_cstride + o * a.outer_out + q + in_blk] = x;
       else dst[(int64_t)(n >> a.split_shift_out) * a.split_stride_out + in_blk] = x;
     }
+  }
   }
 }
 

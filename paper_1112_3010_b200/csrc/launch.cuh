@@ -94,14 +94,22 @@ inline int persist_mode() {
 template <int L, int IN, int OUT>
 constexpr bool tmem_has_lm() { return L >= 10 && L <= 12 && IN == IN_DENSE && (OUT == OUT_COMPS || OUT == OUT_SUM); }
 
+template <int L, int IN, int OUT, bool HALF, bool LM>
+int launch_tmem_persistent_t(const ColArgs& a, int64_t items, cudaStream_t st);
+
 template <int L, int IN, int OUT, bool HALF>
 int launch_tmem_persistent(const ColArgs& a, int64_t items, cudaStream_t st) {
-  using C = TmCfg<L, tm_lpcx(L, OUT)>;
-  auto k = col_tmem_kernel<L, IN, OUT, HALF, false>;
   if (a.ks[0].ls) {
-    if constexpr (tmem_has_lm<L, IN, OUT>()) k = col_tmem_kernel<L, IN, OUT, HALF, true>;
+    if constexpr (tmem_has_lm<L, IN, OUT>()) return launch_tmem_persistent_t<L, IN, OUT, HALF, true>(a, items, st);
     else return fail(EIK_EVALIDATION, "line-major kernel spectra: no column kernel for this shape");
   }
+  return launch_tmem_persistent_t<L, IN, OUT, HALF, false>(a, items, st);
+}
+
+template <int L, int IN, int OUT, bool HALF, bool LM>
+int launch_tmem_persistent_t(const ColArgs& a, int64_t items, cudaStream_t st) {
+  using C = TmCfg<L, tm_lpcx(L, OUT), LM>;
+  auto k = col_tmem_kernel<L, IN, OUT, HALF, LM>;
   const size_t smem_max = C::SMEM_BYTES + ((EIK_DBG_STAGEONLY || C::TSTORE) && L == 12 ? 256 + (size_t)(C::LN::M / 2) * C::LPC * 16 : 0);
   CK(prep_kernel_attr(k, smem_max));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;

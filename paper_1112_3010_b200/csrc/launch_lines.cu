@@ -2,12 +2,19 @@
 
 template <int L, bool INV, bool HALF>
 int launch_lines_t(const LinesArgs& a, int ncomp, cudaStream_t st) {
-  using C = ColCfg<L>;
+  using C = LinesCfg<L>;
   auto k = lines_kernel<L, INV, HALF>;
   CK(prep_kernel_attr(k, C::SMEM_BYTES));
   const int64_t tiles = (a.nlines + C::LPC - 1) / C::LPC;
-  if (tiles <= 0) return EIK_OK;
-  k<<<dim3((unsigned)tiles, (unsigned)ncomp), C::NT, C::SMEM_BYTES, st>>>(a);
+  if (tiles <= 0 || ncomp <= 0) return EIK_OK;
+  const int64_t total = tiles * ncomp;
+  if (total > 0x7fffffffLL) return fail(EIK_EVALIDATION, "too many line tiles in one launch");
+  LinesArgs b = a;
+  b.tiles = tiles;
+  b.ncomp = ncomp;
+  const int64_t wave = sm_count();  // 512-thread persistent CTAs: one per SM
+  const int64_t grid = (C::PERSIST && persist_mode() != 0 && total > wave) ? wave : total;
+  k<<<(unsigned)grid, C::NT, C::SMEM_BYTES, st>>>(b);
   CK(cudaGetLastError());
   return EIK_OK;
 }
