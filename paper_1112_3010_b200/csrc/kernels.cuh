@@ -93,9 +93,15 @@ __host__ __device__ constexpr int col_pad(int L, bool pair) {
 #ifndef EIK_TM11_NT
 #define EIK_TM11_NT 256
 #endif
+#ifndef EIK_TM10_NT
+#define EIK_TM10_NT 256  // A/B: 512 = 8 lines per CTA for the 2-D 1024-point column kernels too
+#endif
+#ifndef EIK_TM9_NT
+#define EIK_TM9_NT 256  // A/B: 512 = 16 lines per CTA for 512-point lines
+#endif
 __host__ __device__ constexpr int tm_pad(int L, bool pair, bool wide = false) {
   return pair ? il2_pad(L, 16)
-       : L == 10 ? (wide ? pad_code(2, 0, 0) : pad_code(2, 4, 0))
+       : L == 10 ? ((wide || EIK_TM10_NT == 512) ? pad_code(2, 0, 0) : pad_code(2, 4, 0))
        : L == 11 ? ((wide || EIK_TM11_NT == 512) ? pad_code(3, 4, 0) : pad_code(3, 5, 6))
        : L == 12 ? pad_code(4, 0, 0)
        : L == 13 ? pad_code(3, 4, 0) : PAD_DEFAULT;
@@ -658,7 +664,9 @@ struct TmCfg {
   static constexpr bool F4K = (L == 12 && EIK_FOUR_STEP && E == 16);
   static constexpr int NT = F4K ? 256 * LPCX : E == 8 ? (L >= 12 ? 1024 : 512)
                             : (WIDE && E == 16 && (L == 10 || L == 11)) ? 512
-                            : (L == 11 && E == 16) ? EIK_TM11_NT : (TPL0 > 256 ? TPL0 : 256);
+                            : (L == 11 && E == 16) ? EIK_TM11_NT
+                            : (L == 10 && E == 16) ? EIK_TM10_NT
+                            : (L == 9 && E == 16) ? EIK_TM9_NT : (TPL0 > 256 ? TPL0 : 256);
   static constexpr int LPC = NT / TPL0;
   static constexpr int MINB = E == 8 ? (NT >= 1024 ? 1 : 2) : (NT >= 512 ? 1 : 2);
   // four-step lines: EIK_F4K_IL = 1 makes the CTA line-major (warps 0-7 line 0,

@@ -14,20 +14,22 @@ lib = sys.argv[1] if len(sys.argv) > 1 else "paper_1112_3010_b200/_lib/libeikfld
 out = sys.argv[2] if len(sys.argv) > 2 else "profiles/round2/sass"
 os.makedirs(out, exist_ok=True)
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
-want = [("col_tmem_12_dense_comps", r"col_tmem_kernelILi12ELi1ELi0ELb1E", "C2 distance column kernel"),
-        ("col_tmem_12_dense_sum", r"col_tmem_kernelILi12ELi1ELi1ELb1E", "C2 sign column kernel"),
+want = [("col_tmem_12_dense_comps", r"col_tmem_kernelILi12ELi1ELi0ELb1ELb0E", "C2 distance column kernel"),
+        ("col_tmem_12_dense_sum", r"col_tmem_kernelILi12ELi1ELi1ELb1ELb0E", "C2 sign column kernel"),
         ("row_11_rcp", r"row_kernelILi11ELb1EE", "C2 row kernel (Hessian epilogue)"),
         ("impulse_rows_1_8", r"impulse_rows_kernelILi1ELi8EE", "row DFT of delta_Y"),
         ("impulse_rows_2_8", r"impulse_rows_kernelILi2ELi8EE", "row DFT of the tangent fields"),
-        ("col_tmem_9_dense_comps", r"col_tmem_kernelILi9ELi1ELi0ELb1E", "C3 axis-0 kernel"),
+        ("col_tmem_9_dense_comps", r"col_tmem_kernelILi9ELi1ELi0ELb1ELb0E", "C3 axis-0 kernel"),
         ("lines_9_inv", r"lines_kernelILi9ELb1ELb0EE", "C3 axis-1 inverse"),
         ("lines_9_fwd_half", r"lines_kernelILi9ELb0ELb1EE", "C3 axis-1 forward (half-padded)"),
         ("row_8", r"row_kernelILi8ELb0EE", "C3 row kernel"),
-        ("col_tmem_10_dense_comps", r"col_tmem_kernelILi10ELi1ELi0ELb1E", "C5 column kernel"),
+        ("col_tmem_10_dense_comps", r"col_tmem_kernelILi10ELi1ELi0ELb1ELb0E", "C5 column kernel"),
         ("row_9", r"row_kernelILi9ELb0EE", "C5 row kernel"),
-        ("col_tmem_11_dense_comps", r"col_tmem_kernelILi11ELi1ELi0ELb1E", "C4 axis-0 kernel (1024^3)"),
-        ("col_tmem_11_dense_sum", r"col_tmem_kernelILi11ELi1ELi1ELb1E", "C4 fused sign axis-0 kernel (slab ranks)"),
-        ("lines_11_inv", r"lines_kernelILi11ELb1ELb0EE", "C4 axis-1 inverse"),
+        ("col_tmem_11_dense_comps_lm", r"col_tmem_kernelILi11ELi1ELi0ELb1ELb1E", "C4 axis-0 kernel (1024^3; line-major spectra, 4 lines per CTA)"),
+        ("col_tmem_11_dense_sum_lm", r"col_tmem_kernelILi11ELi1ELi1ELb1ELb1E", "C4 fused sign axis-0 kernel (slab ranks; line-major spectra)"),
+        ("col_tmem_10_dense_comps_lm", r"col_tmem_kernelILi10ELi1ELi0ELb1ELb1E", "C4@512^3 axis-0 kernel (line-major spectra, 8 lines per CTA)"),
+        ("lines_11_inv", r"lines_kernelILi11ELb1ELb0EE", "C4 axis-1 inverse (16 values per thread, persistent)"),
+        ("lines_11_fwd_half", r"lines_kernelILi11ELb0ELb1EE", "C4 axis-1 forward (half-padded; 16 values per thread, persistent)"),
         ("row_10", r"row_kernelILi10ELb0EE", "C4 row kernel")]
 funcs = re.split(r"\n\s*Function : ", sass)
 index = []
