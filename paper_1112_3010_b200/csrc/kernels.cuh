@@ -1252,6 +1252,12 @@ struct LinesArgs {
 #ifndef EIK_LINES_E16
 #define EIK_LINES_E16 1
 #endif
+// next-tile L2 prefetch from the persistent loop (C4 1024^3: lines passes 19.0 / 19.7 -> 17.8 /
+// 18.5 ms, step 649 -> 638 ms; the same prefetch in the axis-0 column kernel, EIK_NEXTPF, costs
+// 7%: 649 -> 696 ms)
+#ifndef EIK_LINES_NEXTPF
+#define EIK_LINES_NEXTPF 1
+#endif
 template <int L>
 struct LinesCfg16 {
   static constexpr int TPL0 = (1 << L) / 16;
@@ -1309,6 +1315,25 @@ __global__ void __launch_bounds__(LinesCfg<L>::NT) lines_kernel(const __grid_con
     v[r] = (valid && e < a.n_valid)
                ? src[(int64_t)(e >> a.split_shift) * a.split_stride + (int64_t)(e & ((1 << a.split_shift) - 1)) * a.es_in]
                : make_double2(0.0, 0.0);
+  }
+  if constexpr (CC::PERSIST && EIK_LINES_NEXTPF) {
+    // the tile this CTA runs next heads for L2 while this one is transformed (no registers held)
+    const int64_t w2 = w + gridDim.x;
+    if (w2 < total) {
+      const int c2 = (int)(w2 / a.tiles);
+      const int64_t l2 = (w2 - c2 * a.tiles) * LPC + line;
+      if (l2 < a.nlines) {
+        const double2* src2 = a.in[c2] + (l2 / a.inner) * a.outer_in + (l2 % a.inner);
+#pragma unroll
+        for (int r = 0; r < LN::EPT; ++r) {
+          if (HALF && LN::L > 0 && LN::upper_in(r)) continue;
+          const int e = INV ? LN::out_idx(t, r) : LN::in_idx(t, r);
+          if (e < a.n_valid)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(src2 + (int64_t)(e >> a.split_shift) * a.split_stride +
+                                                         (int64_t)(e & ((1 << a.split_shift) - 1)) * a.es_in));
+        }
+      }
+    }
   }
   fft_line<LN, INV, HALF>(v, t, xb, tws);
   if (!valid) continue;
