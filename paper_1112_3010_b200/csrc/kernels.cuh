@@ -1273,9 +1273,14 @@ struct LinesCfg16 {
   static constexpr size_t MB_OFF = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
   static constexpr size_t SMEM_BYTES = MB_OFF + 128;
 };
+// persistent CTAs (+ next-tile prefetch) for the 512-point lines of C3 as well: lines pass
+// 0.812 -> 0.781 ms, step 3.114 -> 3.070 ms
+#ifndef EIK_LINES9_PERSIST
+#define EIK_LINES9_PERSIST 1
+#endif
 template <int L>
 struct LinesColCfg : ColCfg<L> {
-  static constexpr bool PERSIST = false;
+  static constexpr bool PERSIST = (L == 9 && EIK_LINES9_PERSIST);
 };
 template <int L>
 using LinesCfg = std::conditional_t<(EIK_LINES_E16 && L >= 10 && L <= 12), LinesCfg16<L>, LinesColCfg<L>>;

@@ -12,7 +12,7 @@ int launch_lines_t(const LinesArgs& a, int ncomp, cudaStream_t st) {
   LinesArgs b = a;
   b.tiles = tiles;
   b.ncomp = ncomp;
-  const int64_t wave = sm_count();  // 512-thread persistent CTAs: one per SM
+  const int64_t wave = (int64_t)sm_count() * (C::NT >= 512 ? 1 : 512 / C::NT);  // 16 resident warps per SM
   const int64_t grid = (C::PERSIST && persist_mode() != 0 && total > wave) ? wave : total;
   k<<<(unsigned)grid, C::NT, C::SMEM_BYTES, st>>>(b);
   CK(cudaGetLastError());

@@ -51,3 +51,20 @@ def test_single_rank_dry_run_c2():
     line = _dry("--config", "C2")
     assert line["n_gpus"] == 1 and line["grid_points_per_step_job"] == 2048 * 2048
     assert "replicas" in line["config"]["parallelism"]
+
+
+def test_c4_step_bytes_model():
+    """The C4 roofline's byte model: the fused-schedule pass model of DESIGN section 4, summed by hand."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    c, M = (1024, 1024, 1024), (2048, 2048, 2048)
+    H = M[2] // 2 + 1
+    ks = (M[0] // 2 + 1) * (M[1] // 2 + 1) * H * 8
+    plane, slab, N = 16 * c[0] * M[1] * H, 16 * c[0] * c[1] * H, c[0] * c[1] * c[2]
+    want = (2 * slab + 2 * plane) + 4 * (ks + 2 * plane + 2 * slab + 8 * N)
+    want += 3 * (2 * slab + 2 * plane + ks) + 2 * plane + 2 * slab + 9 * N
+    got = bench.c4_step_bytes(c, M)
+    assert got == want
+    # between the compulsory output bytes and SURVEY 8(d)'s looser 1640 B/pt
+    assert 41 * N < got < bench.SURVEY_BYTES_PER_POINT["C4"] * N
