@@ -1844,6 +1844,13 @@ constexpr int ROWDFT_NT = 256;
 #ifndef EIK_T_NPASS
 #define EIK_T_NPASS 2
 #endif
+// Row-fastest lane mapping for the transposed layout (a warp's store of one frequency is one
+// run of rpb rows).  Measured with EIK_T_TRANSPOSE=1, EIK_F4K_LPC_SUM=1: C2 sign pass 0.217 ms
+// -> 0.258 (4 rows per CTA) / 0.40 (8 rows): the extra frequency passes cost the row DFT more
+// than the contiguous column loads save; off.
+#ifndef EIK_T_REMAP
+#define EIK_T_REMAP 0
+#endif
 #ifndef EIK_T_NPASS_RM
 #define EIK_T_NPASS_RM 4
 #endif
@@ -1870,7 +1877,10 @@ __global__ void __launch_bounds__(ROWDFT_NT) impulse_rows_kernel(const __grid_co
   const int npass = a.npass;
   const int tpr = (int)((a.H - 1) / (NF * npass));
   const int rpb = ROWDFT_NT / tpr;
-  const int rl = threadIdx.x / tpr, tl = threadIdx.x % tpr;
+  // transposed output ([k][row]): the CTA's rows run fastest across lanes, so a warp's store
+  // of one frequency is one contiguous run of rpb rows
+  const bool tt = a.out_rs == 1 && EIK_T_REMAP;
+  const int rl = tt ? threadIdx.x % rpb : threadIdx.x / tpr, tl = tt ? threadIdx.x / rpb : threadIdx.x % tpr;
   const int ROWDFT_CHUNK = ROWDFT_STAGE / rpb;  // per row
   const int64_t item = blockIdx.y;
   const int64_t row = (int64_t)blockIdx.x * rpb + rl;
