@@ -152,13 +152,18 @@ __global__ void dd_impulse_kernel(const int64_t* __restrict__ nodes, int64_t K, 
 
 // One radix-2 DIT transform per CTA of the line l: elements base + e * inner,
 // base = (l / inner) * M * inner + (l % inner).
+// Pruned passes (wc < wM): only the lines whose index on the nearest lower axis lies inside the
+// grid window [0, wc) of its wM padded points are transformed (the launch enumerates those);
+// the others are all-zero inputs of a forward pass or unused outputs of an inverse pass.
 template <bool INV>
 __global__ void __launch_bounds__(DD_NT) dd_lines_kernel(double4* data, int L, int64_t inner, const double4* tw,
-                                                         int lmax) {
+                                                         int lmax, int64_t wc, int64_t wM) {
   extern __shared__ double4 sl[];
   const int M = 1 << L;
   const int64_t l = blockIdx.x;
-  const int64_t base = (l / inner) * ((int64_t)M * inner) + (l % inner);
+  const int64_t op = l / inner;
+  const int64_t outer = (op / wc) * wM + (op % wc);
+  const int64_t base = outer * ((int64_t)M * inner) + (l % inner);
   for (int e = threadIdx.x; e < M; e += blockDim.x) {
     const int be = L ? (int)(__brev((unsigned)e) >> (32 - L)) : 0;
     sl[be] = data[base + (int64_t)e * inner];
@@ -271,18 +276,30 @@ struct eik_dd_plan {
 
 namespace {
 
-int dd_transform(eik_dd_plan* p, double4* a, bool inv, cudaStream_t st) {
-  for (int ax = p->D - 1; ax >= 0; --ax) {
-    int64_t inner = 1;
+// window = false: full transform of every line (kernel spectra).  window = true: the input of
+// a forward transform is zero outside the grid window [0, c) per axis and only that window of
+// an inverse transform is read, so the forward runs the last axis first and the inverse the
+// first axis first, each pass skipping the lines that lie outside the window on the axes the
+// other passes have not touched yet / have already finished (2-D: 3/4 of the line transforms,
+// 3-D: 7/12).
+int dd_transform(eik_dd_plan* p, double4* a, bool inv, cudaStream_t st, bool window = false) {
+  for (int step = 0; step < p->D; ++step) {
+    const int ax = (inv && window) ? step : p->D - 1 - step;
+    int64_t inner = 1, outer = 1;
     for (int b = ax + 1; b < p->D; ++b) inner *= p->M[b];
-    const int64_t lines = p->P / p->M[ax];
+    for (int b = 0; b < ax; ++b) outer *= window ? p->c[b] : p->M[b];
+    const int64_t wc = (window && ax > 0) ? p->c[ax - 1] : 1, wM = (window && ax > 0) ? p->M[ax - 1] : 1;
+    const int64_t lines = outer * inner;
+    if (lines > 0x7fffffffLL) return fail(EIK_EVALIDATION, "too many lines in one double-double pass");
     const size_t smem = (size_t)p->M[ax] * sizeof(double4);
     if (inv) {
       CK(prep_kernel_attr(dd_lines_kernel<true>, smem));
-      dd_lines_kernel<true><<<(unsigned)lines, DD_NT, smem, st>>>(a, p->L[ax], inner, p->tw.as<double4>(), p->lmax);
+      dd_lines_kernel<true><<<(unsigned)lines, DD_NT, smem, st>>>(a, p->L[ax], inner, p->tw.as<double4>(), p->lmax, wc,
+                                                                  wM);
     } else {
       CK(prep_kernel_attr(dd_lines_kernel<false>, smem));
-      dd_lines_kernel<false><<<(unsigned)lines, DD_NT, smem, st>>>(a, p->L[ax], inner, p->tw.as<double4>(), p->lmax);
+      dd_lines_kernel<false><<<(unsigned)lines, DD_NT, smem, st>>>(a, p->L[ax], inner, p->tw.as<double4>(), p->lmax, wc,
+                                                                   wM);
     }
     CK(cudaGetLastError());
   }
@@ -407,7 +424,7 @@ int eik_dd_run(eik_dd_plan* p, const int64_t* nodes, int64_t n_nodes, const eik_
   dd_impulse_kernel<<<grid_blocks(n_nodes), 256, 0, st>>>(d_nodes, n_nodes, p->D, p->c[0], p->c[1], p->c[2], p->M[1],
                                                          p->M[2], p->N, X, p->err.as<int>());
   CK(cudaGetLastError());
-  int rc = dd_transform(p, X, false, st);
+  int rc = dd_transform(p, X, false, st, true);
   if (rc) return rc;
   // components: phi, then the gradient / Hessian numerators when requested
   const bool want_grad = o->grad[0] || o->grad[1] || o->grad[2] || o->hess[0];
@@ -418,7 +435,7 @@ int eik_dd_run(eik_dd_plan* p, const int64_t* nodes, int64_t n_nodes, const eik_
   for (int j = 0; j < ncomp; ++j) {
     dd_product_kernel<<<grid_blocks(p->P), 256, 0, st>>>(p->ks.as<double4>() + (int64_t)j * p->P, X, Y, p->P);
     CK(cudaGetLastError());
-    if ((rc = dd_transform(p, Y, true, st))) return rc;
+    if ((rc = dd_transform(p, Y, true, st, true))) return rc;
     dd_extract_kernel<<<grid_blocks(p->N), 256, 0, st>>>(Y, p->D, p->c[1], p->c[2], p->M[1], p->M[2], p->N, log2P,
                                                          fld + (int64_t)j * p->N);
     CK(cudaGetLastError());
