@@ -1384,8 +1384,33 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       ro.n = 1;
       ro.dest[0] = e.phi_raw;
       if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, &ro))) return rc2;
-      for (int d = 0; d < r.ngrad; ++d) {
-        if (!o_g[d]) continue;
+      // gradient components: one axis-0 pass each, except the last two, which share one pass
+      // (one forward transform and one read of V fewer): V is dead after them, so the first of
+      // the pair lands in V's own lines (every CTA reads its lines before it writes them) and
+      // the second in W.  Same arithmetic per component as the single passes (bit-identical).
+      int gd[3], ng = 0;
+      for (int d = 0; d < r.ngrad; ++d)
+        if (o_g[d]) gd[ng++] = d;
+      static const bool pair_last = [] {
+        const char* ev = std::getenv("EIK_STREAM_PAIR");
+        return !(ev && ev[0] == '0');
+      }();
+      for (int i = 0; i < ng; ++i) {
+        const int d = gd[i];
+        if (pair_last && ng >= 2 && i == ng - 2) {
+          const int d2 = gd[i + 1];
+          const KDev* kk[2] = {p->kdist[p->k_grad + d].get(), p->kdist[p->k_grad + d2].get()};
+          double2* WW[2] = {V1, W1};
+          if ((rc2 = pass_axis0_list(p, V1, kk, 2, WW, false, st))) return rc2;
+          RawOut ro2;
+          ro2.n = 2;
+          ro2.dest[0] = o_g[d];
+          ro2.dest[1] = o_g[d2];
+          if ((rc2 = pass_finish(p, WW, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, &ro2))) return rc2;
+          e.grad[d] = o_g[d];
+          e.grad[d2] = o_g[d2];
+          break;
+        }
         if ((rc2 = pass_axis0_single(p, V1, *p->kdist[p->k_grad + d], W1, false, st))) return rc2;
         ro.dest[0] = o_g[d];
         if ((rc2 = pass_finish(p, &W1, r, p->c[0], p->M[1], 1, rr, st, nomark, nullptr, &ro))) return rc2;
