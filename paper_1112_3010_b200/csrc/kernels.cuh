@@ -747,6 +747,15 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 #ifndef EIK_DBG_NOK
 #define EIK_DBG_NOK 0
 #endif
+// accumulating 3-D passes prefetch their destination rows into L2 before the inverse
+// transform (C4 1024^3: sign group 287 -> 276.5 ms)
+#ifndef EIK_ACCUM_PF
+#define EIK_ACCUM_PF 1
+#endif
+// (C4 1024^3: 612.7 -> 602.3 ms in one A/B, within 3 ms of run-to-run noise)
+#ifndef EIK_LM_KPF_EARLY
+#define EIK_LM_KPF_EARLY 1
+#endif
 #ifndef EIK_DBG_NOST
 #define EIK_DBG_NOST 0
 #endif
@@ -918,13 +927,19 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT), LM>::NT, TmCfg<L, tm
         }
       }
     } else {
+      // 3-D passes often carry one component (streamed schedule): its kernel spectrum heads
+      // for L1 before the forward transform, not after it
+      constexpr bool KPF_EARLY = LM && EIK_LM_KPF_EARLY;
+      if constexpr (KPF_EARLY) {
+        if (valid && !EIK_DBG_NOK) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
+      }
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
       fft_line<LN, false, HALF>(v, t, xb, tws);
       tmem_put(ta, v);
       // kernel spectra: the next component's lines are prefetched into L1 one
       // transform ahead (no registers held across the FFT); loaded at use
-      if (valid && !EIK_DBG_NOK) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
+      if (!KPF_EARLY && valid && !EIK_DBG_NOK) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
       next_prefetch();
 #pragma unroll 1
       for (int j = 0; j < a.n_comp; ++j) {
@@ -934,6 +949,17 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT), LM>::NT, TmCfg<L, tm
           kload_all<TC, LM>(kn, a.ks[j], lk, t, bx);
           if (j + 1 < a.n_comp) kprefetch_all<TC, LM>(a.ks[j + 1], lk, t, bx);
           kapply_all<LN>(v, kn, a.ks[j], t, mir);
+        }
+        if constexpr (LM && EIK_ACCUM_PF) {
+          // accumulating pass: the destination rows head for L2 while the inverse runs
+          if (a.accum && valid) {
+#pragma unroll
+            for (int r = 0; r < LN::EPT; ++r) {
+              if (LN::L > 0 && LN::upper_in(r)) continue;
+              const int n = LN::in_idx(t, r);
+              if (n < a.n_out) asm volatile("prefetch.global.L2 [%0];" ::"l"(comp_dst(a, j, item, l, n)));
+            }
+          }
         }
         fft_line<LN, true>(v, t, xb, tws);
         if (a.accum) {  // uniform: the streamed sign group adds into W
