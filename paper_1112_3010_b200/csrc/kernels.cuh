@@ -756,6 +756,9 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 #ifndef EIK_LM_KPF_EARLY
 #define EIK_LM_KPF_EARLY 1
 #endif
+#ifndef EIK_KPF_EARLY_ALL
+#define EIK_KPF_EARLY_ALL 0  // the same for the 2-D kernels (6 / 3 components per pass): C2 column kernel 0.318 -> 0.326 ms, C5 4.68 -> 4.73, C3 equal (the early lines do not survive in L1 next to the input loads)
+#endif
 #ifndef EIK_DBG_NOST
 #define EIK_DBG_NOST 0
 #endif
@@ -929,7 +932,7 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT), LM>::NT, TmCfg<L, tm
     } else {
       // 3-D passes often carry one component (streamed schedule): its kernel spectrum heads
       // for L1 before the forward transform, not after it
-      constexpr bool KPF_EARLY = LM && EIK_LM_KPF_EARLY;
+      constexpr bool KPF_EARLY = (LM && EIK_LM_KPF_EARLY) || EIK_KPF_EARLY_ALL;
       if constexpr (KPF_EARLY) {
         if (valid && !EIK_DBG_NOK) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
       }
