@@ -1014,17 +1014,68 @@ struct StreamEpi {
 
 // Elementwise epilogue of the streamed schedule: the operations of row_kernel's
 // fused epilogue (3-D: no Hessian, ratios by division) on the raw fields.
-__global__ void stream_epilogue_kernel(const StreamEpi e) {
+// every double field 16-byte aligned (null fields count as aligned): the vector path applies
+inline int stream_epi_vec2(const StreamEpi& e) {
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return al16(e.phi_raw) && al16(e.S) && al16(e.phi_out) && al16(e.grad[0]) && al16(e.grad[1]) && al16(e.grad[2]) &&
+         al16(e.mu_raw) && al16(e.mu);
+}
+// One element of the streamed epilogue (same double operations as the fused row epilogue).
+__device__ __forceinline__ void stream_epi_dist(const StreamEpi& e, double phi, double (&g)[3], double& S, unsigned& cnt) {
+  cnt += (phi <= 0.0);
+  for (int d = 0; d < 3; ++d)
+    if (e.grad[d]) g[d] = g[d] / phi;
+  S = phi > 0.0 ? (-e.tau) * log(phi) : __longlong_as_double(0x7ff8000000000000LL);
+}
+// Two elements per thread and iteration through 16-byte loads / stores when every field is
+// 16-byte aligned (C4 1024^3: 23.3 ms of scalar accesses at 57% of the HBM peak before)
+__global__ void stream_epilogue_kernel(const StreamEpi e, int vec2) {
   unsigned cnt = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e.N; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t npair = vec2 ? e.N / 2 : 0;
+  for (int64_t q = tid0; q < npair; q += stride) {
+    const int64_t i = 2 * q;
+    if (e.phi_raw) {
+      const double2 phi = *reinterpret_cast<const double2*>(e.phi_raw + i);
+      double2 gv[3];
+      for (int d = 0; d < 3; ++d)
+        if (e.grad[d]) gv[d] = *reinterpret_cast<const double2*>(e.grad[d] + i);
+      double g0[3] = {gv[0].x, gv[1].x, gv[2].x}, g1[3] = {gv[0].y, gv[1].y, gv[2].y};
+      double S0, S1;
+      stream_epi_dist(e, phi.x, g0, S0, cnt);
+      stream_epi_dist(e, phi.y, g1, S1, cnt);
+      for (int d = 0; d < 3; ++d)
+        if (e.grad[d]) *reinterpret_cast<double2*>(e.grad[d] + i) = make_double2(g0[d], g1[d]);
+      if (e.phi_out && e.phi_out != e.phi_raw) *reinterpret_cast<double2*>(e.phi_out + i) = phi;
+      if (e.uf) {
+        e.uf[i] = phi.x <= 0.0;
+        e.uf[i + 1] = phi.y <= 0.0;
+      }
+      if (e.S) *reinterpret_cast<double2*>(e.S + i) = make_double2(S0, S1);
+    }
+    if (e.mu_raw) {
+      const double2 mr = *reinterpret_cast<const double2*>(e.mu_raw + i);
+      const double m0 = -mr.x / 12.566370614359172, m1 = -mr.y / 12.566370614359172;
+      if (e.mu) *reinterpret_cast<double2*>(e.mu + i) = make_double2(m0, m1);
+      if (e.mask) {
+        e.mask[i] = rint(m0) >= 1.0;
+        e.mask[i + 1] = rint(m1) >= 1.0;
+      }
+    }
+  }
+  for (int64_t i = 2 * npair + tid0; i < e.N; i += stride) {
     if (e.phi_raw) {
       const double phi = e.phi_raw[i];
-      cnt += (phi <= 0.0);
+      double g[3] = {0.0, 0.0, 0.0}, S;
       for (int d = 0; d < 3; ++d)
-        if (e.grad[d]) e.grad[d][i] = e.grad[d][i] / phi;
+        if (e.grad[d]) g[d] = e.grad[d][i];
+      stream_epi_dist(e, phi, g, S, cnt);
+      for (int d = 0; d < 3; ++d)
+        if (e.grad[d]) e.grad[d][i] = g[d];
       if (e.phi_out && e.phi_out != e.phi_raw) e.phi_out[i] = phi;
       if (e.uf) e.uf[i] = phi <= 0.0;
-      if (e.S) e.S[i] = phi > 0.0 ? (-e.tau) * log(phi) : __longlong_as_double(0x7ff8000000000000LL);
+      if (e.S) e.S[i] = S;
     }
     if (e.mu_raw) {
       const double m = -e.mu_raw[i] / 12.566370614359172;
@@ -1439,7 +1490,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       if ((rc2 = mark(EIK_PASS_COL_SIGN, true))) return rc2;
     }
     if ((rc2 = mark(EIK_PASS_ROW, false))) return rc2;
-    stream_epilogue_kernel<<<148 * 8, 256, 0, st>>>(e);
+    stream_epilogue_kernel<<<148 * 8, 256, 0, st>>>(e, stream_epi_vec2(e));
     CK(cudaGetLastError());
     return mark(EIK_PASS_ROW, true);
   };
@@ -1798,7 +1849,7 @@ int eik_slab_epilogue(eik_plan* p, int64_t n_local, const double* phi_raw, const
     e.mu = out->mu;
     e.mask = out->mask;
   }
-  stream_epilogue_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(e);
+  stream_epilogue_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(e, stream_epi_vec2(e));
   CK(cudaGetLastError());
   return EIK_OK;
 }
