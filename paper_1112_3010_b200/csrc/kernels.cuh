@@ -1284,6 +1284,9 @@ struct LinesArgs {
 // next-tile L2 prefetch from the persistent loop (C4 1024^3: lines passes 19.0 / 19.7 -> 17.8 /
 // 18.5 ms, step 649 -> 638 ms; the same prefetch in the axis-0 column kernel, EIK_NEXTPF, costs
 // 7%: 649 -> 696 ms)
+#ifndef EIK_LINES16_SPLIT
+#define EIK_LINES16_SPLIT 1  // split-phase exchange barriers in the 16-value lines kernels (C4 1024^3: 596 -> 586.5 ms)
+#endif
 #ifndef EIK_LINES_NEXTPF
 #define EIK_LINES_NEXTPF 1
 #endif
@@ -1298,7 +1301,7 @@ struct LinesCfg16 {
   __device__ static __forceinline__ int line_of(int tid) { return tid % LPC; }
   __device__ static __forceinline__ int t_of(int tid) { return tid / LPC; }
   static constexpr int NBUF = 1;
-  using XB = XBuf<1, 0, NT, false>;
+  using XB = XBuf<1, 0, NT, (EIK_LINES16_SPLIT != 0)>;
   static constexpr size_t MB_OFF = ((size_t)LPC * LN::SMEM + LN::TWQ + LN::ST_SIZE) * sizeof(double2);
   static constexpr size_t SMEM_BYTES = MB_OFF + 128;
 };
