@@ -726,6 +726,53 @@ struct TmCfg {
   static constexpr size_t SMEM_TSTORE_BYTES = TSTORE_OFF + 128 + TSTORE_TILE + 32;
 };
 
+#ifndef EIK_SUM_CHUNKED
+#define EIK_SUM_CHUNKED 0  // measured: ptxas spills more (132 / 252 bytes against 84 / 120)
+#endif
+#ifndef EIK_SUM_KCHUNK
+#define EIK_SUM_KCHUNK 0  // measured: spill loads 120 -> 100 bytes, but the C2 sign pass 0.217 -> 0.225 ms
+#endif
+// v[r] *= K, four kernel-spectrum values at a time (sign group: the running sum, the product
+// and 16 spectrum values do not fit 128 registers together)
+template <class CFG, bool LM>
+__device__ __forceinline__ void kmul_chunked(double2 (&v)[16], const KSpec& k, int64_t l, int t, int64_t bx, bool mir) {
+  using LN = typename CFG::LN;
+  const double* __restrict__ src = k.perm ? k.perm + bx * LN::EPT * CFG::NTP + threadIdx.x : nullptr;
+  const bool neg1 = k.odd1 && mir;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double kn[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 4 * c + q;
+      kn[q] = (!LM && src) ? __ldg(src + r * CFG::NTP) : kload<LM>(k, l, LN::out_idx(t, r), LN::M);
+      if ((k.odd0 && LN::out_idx(t, r) > (LN::M >> 1)) != neg1) kn[q] = -kn[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 4 * c + q;
+      v[r] = k.imag ? make_double2(-v[r].y * kn[q], v[r].x * kn[q]) : make_double2(v[r].x * kn[q], v[r].y * kn[q]);
+    }
+    asm volatile("" ::: "memory");
+  }
+}
+// v[i] = y[i] + v[i] with the 16 complex values y at TMEM address a, four at a time
+__device__ __forceinline__ void tmem_add16(uint32_t a, double2 (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t w32[16];
+    tmem_ld16(a + 16 * c, w32);
+    tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 y = make_double2(
+          __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 1] << 32) | w32[4 * q])),
+          __longlong_as_double((long long)(((unsigned long long)w32[4 * q + 3] << 32) | w32[4 * q + 2])));
+      v[4 * c + q] = cadd(y, v[4 * c + q]);
+    }
+  }
+}
+
 // TMA tensor store (3-D box, shared -> global) and its bulk-group bookkeeping
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
@@ -847,19 +894,27 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT), LM>::NT, TmCfg<L, tm
           if (i + 1 == a.n_in) next_prefetch();
         }
         fft_line<LN, false, HALF>(v, t, xb, tws);
-        double kn[LN::EPT];
         if (valid) {
-          kload_all<TC, LM>(kn, a.ks[i], lk, t, bx);
-          kapply_all<LN>(v, kn, a.ks[i], t, mir);
+          if constexpr (EIK_SUM_KCHUNK && LN::EPT == 16 && !TC::PFOLD) {
+            kmul_chunked<TC, LM>(v, a.ks[i], lk, t, bx, mir);
+          } else {
+            double kn[LN::EPT];
+            kload_all<TC, LM>(kn, a.ks[i], lk, t, bx);
+            kapply_all<LN>(v, kn, a.ks[i], t, mir);
+          }
         } else {
 #pragma unroll
           for (int r = 0; r < LN::EPT; ++r) v[r] = make_double2(0.0, 0.0);
         }
         if (i > 0) {
-          double2 y[LN::EPT];
-          tmem_get(ta, y);
+          if constexpr (EIK_SUM_CHUNKED && LN::EPT == 16) {
+            tmem_add16(ta, v);  // four values at a time: the running sum never sits in 64 registers
+          } else {
+            double2 y[LN::EPT];
+            tmem_get(ta, y);
 #pragma unroll
-          for (int r = 0; r < LN::EPT; ++r) v[r] = cadd(y[r], v[r]);
+            for (int r = 0; r < LN::EPT; ++r) v[r] = cadd(y[r], v[r]);
+          }
         }
         if (i + 1 < a.n_in) tmem_put(ta, v);
       }
