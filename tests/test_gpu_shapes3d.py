@@ -44,7 +44,8 @@ def test_small_3d_shapes_vs_oracle(cuda_ok, counts, streamed, monkeypatch):
 # column kernels of those lengths read line-major kernel spectra (KSpec::ls) and run their
 # wide configuration, the axis-1 lines kernels their 16-values-per-thread persistent one
 # (csrc/kernels.cuh: TmCfg<.., WIDE>, LinesCfg16); cheap to check in full against the oracle.
-LONG_SHAPES = [(300, 3, 2), (600, 2, 3), (1100, 2, 2), (2, 300, 3), (3, 600, 2), (2, 1100, 2), (260, 270, 2)]
+LONG_SHAPES = [(300, 3, 2), (600, 2, 3), (1100, 2, 2), (2, 300, 3), (3, 600, 2), (2, 1100, 2), (260, 270, 2),
+               (520, 530, 2), (1030, 12, 5), (12, 1030, 3), (3, 700, 130)]
 
 
 @pytest.mark.parametrize("streamed", ["0", "1"])
