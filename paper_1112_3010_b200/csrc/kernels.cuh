@@ -796,6 +796,13 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 #endif
 // accumulating 3-D passes prefetch their destination rows into L2 before the inverse
 // transform (C4 1024^3: sign group 287 -> 276.5 ms)
+// Skipping the TMEM round trip component 0 does not need (its spectrum is still in the
+// registers the forward transform left) is SLOWER in every kernel: C2 column kernel 0.319 ->
+// 0.329 ms, C5 4.68 -> 4.98, C3 1.54 -> 1.56, C4 587 -> 599 ms per step (the branches around
+// the tcgen05 instructions cost the schedule more than the two transfers); off.
+#ifndef EIK_TM_SKIP0
+#define EIK_TM_SKIP0 0
+#endif
 #ifndef EIK_ACCUM_PF
 #define EIK_ACCUM_PF 1
 #endif
@@ -994,14 +1001,14 @@ __global__ void __launch_bounds__(TmCfg<L, tm_lpcx(L, OUT), LM>::NT, TmCfg<L, tm
       if constexpr (IN == IN_SPARSE) load_sparse<LN, HALF>(v, a, t, l, item, 0, valid, twq);
       else load_dense<LN, HALF>(v, a, t, l, item, 0, valid);
       fft_line<LN, false, HALF>(v, t, xb, tws);
-      tmem_put(ta, v);
+      if (!EIK_TM_SKIP0 || a.n_comp > 1) tmem_put(ta, v);  // one component: the spectrum stays in registers
       // kernel spectra: the next component's lines are prefetched into L1 one
       // transform ahead (no registers held across the FFT); loaded at use
       if (!KPF_EARLY && valid && !EIK_DBG_NOK) kprefetch_all<TC, LM>(a.ks[0], lk, t, bx);
       next_prefetch();
 #pragma unroll 1
       for (int j = 0; j < a.n_comp; ++j) {
-        tmem_get(ta, v);
+        if (!EIK_TM_SKIP0 || j > 0) tmem_get(ta, v);  // component 0 multiplies the registers the forward left
         if (valid && !EIK_DBG_NOK) {
           double kn[LN::EPT];
           kload_all<TC, LM>(kn, a.ks[j], lk, t, bx);
