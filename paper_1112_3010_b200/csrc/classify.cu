@@ -283,6 +283,37 @@ __global__ void fill_fix_kernel(const int64_t* nodes, int64_t K, int rank, FillG
   }
 }
 
+// The search half of the sparse fill: src[i] = flat index of flagged node i's feature (its
+// nearest unflagged node under scipy's tie rules), -1 when it has none.  Depends on the
+// flagged bitmap only, so the pipeline runs it next to the column passes; the apply half
+// (mask[node] = mask[src]) is all that is left after the row pass has classified the nodes.
+__global__ void fill_search_kernel(const int64_t* nodes, int64_t K, int rank, FillGeo g, int64_t* src) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const int64_t v = nodes[i];
+  const int64_t N = (int64_t)g.n[0] * g.n[1] * g.n[2];
+  int64_t out = -1;
+  if (v >= 0 && v < N) {
+    int c[3];
+    c[0] = (int)(v / g.s[0]);
+    c[1] = (int)((v / g.s[1]) % g.n[1]);
+    c[2] = (int)(v % g.n[2]);
+    int f[3];
+    bool ok;
+    if (rank == 1) ok = fill_feature<0>(g, c, f);
+    else if (rank == 2) ok = fill_feature<1>(g, c, f);
+    else ok = fill_feature<2>(g, c, f);
+    if (ok) out = (f[0] - g.e0) * g.s[0] + f[1] * g.s[1] + f[2] * g.s[2];
+  }
+  src[i] = out;
+}
+__global__ void fill_apply_kernel(const int64_t* nodes, const int64_t* src, int64_t K, uint8_t* mask) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const int64_t s = src[i];
+  if (s >= 0) mask[nodes[i]] = mask[s];  // features are unflagged nodes: never written here
+}
+
 FillGeo fill_geo(int dim, const int64_t* counts, const uint32_t* bits, int* oob) {
   FillGeo g{};
   g.n[0] = g.n[1] = g.n[2] = 1;
@@ -377,6 +408,27 @@ __global__ void fill_copy_dense_kernel(const int64_t* nodes, int64_t K, const in
 int eik_fill_bits(const int64_t* d_nodes, int64_t K, int64_t N, uint32_t* bits, cudaStream_t st) {
   CKC(cudaMemsetAsync(bits, 0, ((N + 31) / 32) * sizeof(uint32_t), st));
   if (K > 0) fill_bits_kernel<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(d_nodes, K, N, bits, nullptr);
+  CKC(cudaGetLastError());
+  return EIK_OK;
+}
+
+// Sparse flagged sets only (the rule eik_fill_mask applies): true when the split fill is used
+bool eik_fill_is_sparse(int dim, const int64_t* counts, int64_t K) {
+  int64_t N = 1;
+  for (int a = 0; a < dim; ++a) N *= counts[a];
+  return K > 0 && K <= N / 8;
+}
+int eik_fill_search(int dim, const int64_t* counts, const int64_t* d_nodes, int64_t K, const uint32_t* bits,
+                    int64_t* src, cudaStream_t st) {
+  if (K <= 0) return EIK_OK;
+  const FillGeo g = fill_geo(dim, counts, bits, nullptr);
+  fill_search_kernel<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(d_nodes, K, dim, g, src);
+  CKC(cudaGetLastError());
+  return EIK_OK;
+}
+int eik_fill_apply(const int64_t* d_nodes, const int64_t* src, int64_t K, uint8_t* mask, cudaStream_t st) {
+  if (K <= 0) return EIK_OK;
+  fill_apply_kernel<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(d_nodes, src, K, mask);
   CKC(cudaGetLastError());
   return EIK_OK;
 }

@@ -36,6 +36,10 @@ int eik_fail(int code, const std::string& msg) {
 
 // classify.cu: flagged-node fill of the sign mask (R/sign.py:179-189)
 int eik_fill_bits(const int64_t* d_nodes, int64_t K, int64_t N, uint32_t* bits, cudaStream_t st);
+bool eik_fill_is_sparse(int dim, const int64_t* counts, int64_t K);
+int eik_fill_search(int dim, const int64_t* counts, const int64_t* d_nodes, int64_t K, const uint32_t* bits,
+                    int64_t* src, cudaStream_t st);
+int eik_fill_apply(const int64_t* d_nodes, const int64_t* src, int64_t K, uint8_t* mask, cudaStream_t st);
 int eik_fill_mask(int dim, const int64_t* counts, const int64_t* d_nodes, int64_t K, const uint32_t* bits,
                   uint8_t* mask, cudaStream_t st);
 int eik_slab_fill_mask(const int64_t* counts, const int64_t* ext_nodes, int64_t K, int64_t e0, int64_t e1,
@@ -151,11 +155,13 @@ struct eik_plan {
   cudaEvent_t ev[2 * EIK_NPASS] = {};
   bool ev_used[EIK_NPASS] = {};
   // side stream: the 2-D sign group runs concurrently with the distance group
-  cudaStream_t st2 = nullptr, st_copy = nullptr, st_copy2 = nullptr;
+  cudaStream_t st2 = nullptr, st_copy = nullptr, st_copy2 = nullptr, st3 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk = nullptr, ev_copies = nullptr;
+  cudaEvent_t ev_fill0 = nullptr, ev_fill1 = nullptr;  // side stream of the mask-fill search
   bool copies_pending = false;  // EIK_ASYNC: D2H of the last run still reads `stage`
   DevBuf serr, trows, tsign;
   DevBuf fillbits;  // flagged-node bitmap of the sign nodes (mask fill)
+  DevBuf fillsrc;   // per sign node: flat index of its nearest unflagged node (split fill)
   // peer-to-peer slab exchange: own arena [P2P_NV V slots][n_comp W slots]
   // and every rank's arena base (own, same-process or IPC-opened)
   DevBuf p2p;
@@ -179,6 +185,9 @@ struct eik_plan {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
+    if (ev_fill0) cudaEventDestroy(ev_fill0);
+    if (ev_fill1) cudaEventDestroy(ev_fill1);
+    if (st3) cudaStreamDestroy(st3);
     if (st_copy) cudaStreamDestroy(st_copy);
     if (st_copy2) cudaStreamDestroy(st_copy2);
     if (ev_chunk) cudaEventDestroy(ev_chunk);
@@ -1283,6 +1292,46 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
   const int64_t fill_counts[3] = {p->dim == 1 ? p->c[1] : p->c[0], p->c[1], p->c[2]};
   if (want_fill) CK(p->fillbits.ensure(((p->N + 31) / 32) * sizeof(uint32_t)));
   uint32_t* fbits = p->fillbits.as<uint32_t>();
+  // sparse flagged sets: the nearest-unflagged-node search needs the bitmap only, so it is
+  // queued right behind it (next to the column passes); after the row pass one gather is left
+  // (C2: the 19 us search kernel leaves the tail of the step).  EIK_FILL_SPLIT=0: search at the end.
+  static const bool fill_split_on = [] {
+    const char* e = std::getenv("EIK_FILL_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  const bool fill_split = want_fill && fill_split_on && eik_fill_is_sparse(p->dim, fill_counts, Ks);
+  if (fill_split) CK(p->fillsrc.ensure((size_t)Ks * sizeof(int64_t)));
+  // side = true (2-D, the groups forked onto two streams): bitmap and search run on a third
+  // stream, off both groups' chains (inside a group's stream the search only moves from the
+  // step's tail to its head: measured 0.803 -> 0.810 ms), joined before the apply
+  bool fill_side_pending = false;
+  auto fill_prepare = [&](cudaStream_t s2, bool side = false) -> int {
+    cudaStream_t sf = s2;
+    if (side && fill_split) {
+      if (!p->st3) CK(cudaStreamCreateWithFlags(&p->st3, cudaStreamNonBlocking));
+      if (!p->ev_fill0) CK(cudaEventCreateWithFlags(&p->ev_fill0, cudaEventDisableTiming));
+      if (!p->ev_fill1) CK(cudaEventCreateWithFlags(&p->ev_fill1, cudaEventDisableTiming));
+      CK(cudaEventRecord(p->ev_fill0, s2));
+      CK(cudaStreamWaitEvent(p->st3, p->ev_fill0, 0));
+      sf = p->st3;
+    }
+    int rcf = eik_fill_bits(d_snodes, Ks, p->N, fbits, sf);
+    if (rcf || !fill_split) return rcf;
+    if ((rcf = eik_fill_search(p->dim, fill_counts, d_snodes, Ks, fbits, p->fillsrc.as<int64_t>(), sf))) return rcf;
+    if (sf != s2) {
+      CK(cudaEventRecord(p->ev_fill1, sf));
+      fill_side_pending = true;
+    }
+    return EIK_OK;
+  };
+  auto fill_finish = [&](cudaStream_t s2) -> int {
+    if (fill_side_pending) {
+      CK(cudaStreamWaitEvent(s2, p->ev_fill1, 0));
+      fill_side_pending = false;
+    }
+    if (fill_split) return eik_fill_apply(d_snodes, p->fillsrc.as<int64_t>(), Ks, o_mask, s2);
+    return eik_fill_mask(p->dim, fill_counts, d_snodes, Ks, fbits, o_mask, s2);
+  };
   // EIK_WAVE=n (2-D distance batches on the row-DFT path): items run in waves
   // of n, column pass then row pass per wave, so the wave's T and U_j stay in
   // L2 between the passes instead of round-tripping HBM
@@ -1352,7 +1401,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
       if (!want_sign) return EIK_OK;
       int rc2;
       if ((rc2 = mark(EIK_PASS_COL_SIGN, false))) return rc2;
-      if (want_fill && (rc2 = eik_fill_bits(d_snodes, Ks, p->N, fbits, ss))) return rc2;
+      if (want_fill && (rc2 = fill_prepare(ss, fork))) return rc2;
       if ((rc2 = pass_col2d(p, true, d_snodes, nullptr, Ks, 1, d_sw, r, W.data(), ss))) return rc2;
       if ((rc2 = mark(EIK_PASS_COL_SIGN, true))) return rc2;
       if (fork) CK(cudaEventRecord(p->ev_join, ss));
@@ -1381,7 +1430,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     }
     if (want_sign) {
       if ((rc = mark(EIK_PASS_COL_SIGN, false))) return rc;
-      if (want_fill && (rc = eik_fill_bits(d_snodes, Ks, p->N, fbits, st))) return rc;
+      if (want_fill && (rc = fill_prepare(st))) return rc;
       if ((rc = pass_planes(p, true, d_snodes, nullptr, Ks, 1, d_sw, p->c[0], p->M[1], V, st)))
         return rc;
       if ((rc = pass_axis0(p, true, V, 0, p->M[1], 1, r, W.data(), st))) return rc;
@@ -1475,7 +1524,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     }
     if (want_sign) {
       if ((rc2 = mark(EIK_PASS_COL_SIGN, false))) return rc2;
-      if (want_fill && (rc2 = eik_fill_bits(d_snodes, Ks, p->N, fbits, st))) return rc2;
+      if (want_fill && (rc2 = fill_prepare(st))) return rc2;
       for (int i = 0; i < 3; ++i) {
         if ((rc2 = pass_planes_inplace(p, true, d_snodes, Ks, d_sw + (int64_t)i * Ks, V1, st))) return rc2;
         if ((rc2 = pass_axis0_single(p, V1, *p->ksign[i], W1, i > 0, st))) return rc2;
@@ -1550,7 +1599,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     };
     if ((rc = finish(on_chunk))) return rc;
     if (want_fill) {
-      if ((rc = eik_fill_mask(p->dim, fill_counts, d_snodes, Ks, fbits, o_mask, st))) return rc;
+      if ((rc = fill_finish(st))) return rc;
       CK(cudaEventRecord(p->ev_chunk, st));
       CK(cudaStreamWaitEvent(p->st_copy, p->ev_chunk, 0));
       for (auto& sl : slots)
@@ -1564,7 +1613,7 @@ static int run_locked(eik_plan* p, const eik_inputs* in, const eik_outputs* out,
     slots.clear();
   } else {
     if ((rc = finish(nullptr))) return rc;
-    if (want_fill && (rc = eik_fill_mask(p->dim, fill_counts, d_snodes, Ks, fbits, o_mask, st))) return rc;
+    if (want_fill && (rc = fill_finish(st))) return rc;
   }
   // ---- copy back / sync / checks
   for (auto& s : slots) CK(cudaMemcpyAsync(s.user, s.dev, s.bytes, cudaMemcpyDeviceToHost, st));
