@@ -607,8 +607,9 @@ def main():
 
     # kernels per step (profiles/round2 launch lists): per group prep_nodes +
     # impulse_rows + column pass, then the row pass; C2 adds the sign mask fill
-    # (flag bitmap + per-flagged-node fix-up); 3-D adds the axis-1 lines passes
-    launches_per_step = {"C1": 4, "C2": 9, "C3": 6, "C5": 4}[a.config]
+    # (flag bitmap + per-flagged-node search on a side stream + the gather behind the row
+    # pass); 3-D adds the axis-1 lines passes
+    launches_per_step = {"C1": 4, "C2": 10, "C3": 6, "C5": 4}[a.config]
     if rank == 0:
         line = {
             "metric": "grid points/sec (S+grad S+sign)", "value": value, "unit": "grid_points/s", "n_gpus": world,
